@@ -1,0 +1,358 @@
+"""bench.py -- QFT / TFXY circuit time on B200 through libqc (the C ABI).
+
+Default workload = BASELINE.json configs[1]: TFXY 1D Trotter circuit, 20
+qubits, 10 Trotter steps, complex double, random initial state, 1 B200.
+A "step" is one qc_run_circuit of the whole circuit on the resident state.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config tfxy20|qft10|qft30|qft30c64|tfxy33] [--no-sweep]
+
+Under torchrun (N > 1) every rank runs its own replica of the workload
+("replicas only": the default workload does not shard), timing
+is max over ranks, value = N*K circuits / max time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QFT & TFXY circuit time vs qubits at 1-8 B200; per-gate HBM GB/s vs peak"
+
+CONFIGS = {
+    # name: (family, n, steps, precision, description)
+    "qft10": ("qft", 10, 0, "c128", "QFT on 10 qubits, complex double, random initial state"),
+    "tfxy20": ("tfxy", 20, 10, "c128", "TFXY 1D Trotter circuit, 20 qubits, 10 time steps, complex double, 1 B200"),
+    "qft30": ("qft", 30, 0, "c128", "QFT on 30 qubits, complex double, 1 B200"),
+    "qft30c64": ("qft", 30, 0, "c64", "QFT on 30 qubits, complex single, 1 B200"),
+    "tfxy33": ("tfxy", 33, 10, "c128", "TFXY Trotter circuit, 33 qubits complex double, 1 B200"),
+}
+
+
+def build_ops(cfg):
+    import qcgen
+    fam, n, steps, prec, _ = CONFIGS[cfg]
+    return qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, steps)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(cfg: str, budget_s: float = 15.0):
+    """Time the oracle (as it stands) on the host cores on a bounded prefix of
+    the same circuit; returns circuits/s extrapolated from the prefix."""
+    import oracle
+    import qcgen
+    fam, n, steps, prec, _ = CONFIGS[cfg]
+    ops = build_ops(cfg)
+    n_s = min(n, 24)  # largest size the host holds comfortably for a bounded sample
+    st = qcgen.random_state(n_s, precision=prec)
+    sample_ops = ops if n_s == n else [o for o in ops if max(o.qubits) < n_s]
+    done, t0 = 0, time.perf_counter()
+    psi = st
+    chunk = 8
+    while done < len(sample_ops) and time.perf_counter() - t0 < budget_s:
+        psi = oracle.run(n_s, psi, sample_ops[done:done + chunk])
+        done += min(chunk, len(sample_ops) - done)
+    el = time.perf_counter() - t0
+    per_gate = el / max(done, 1) * (2.0 ** (n - n_s))
+    rate = 1.0 / (per_gate * len(ops))
+    sample = (f"first {done} of {len(ops)} gates of the {cfg} circuit at n={n_s}"
+              + ("" if n_s == n else f", per-gate time scaled x2 per qubit to n={n} (P:112 law)")
+              + f", {el:.1f} s")
+    return rate, oracle.max_threads(), sample
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2303_00123_b200 as qc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    fam, n, steps_c, prec, desc = CONFIGS[args.config]
+    ops = build_ops(args.config)
+    arr = qc.encode_ops(ops)
+    s = qc.State(n, prec, device=local_rank)
+    stream = torch.cuda.ExternalStream(s.stream, device=dev)
+    s.init_random(12345)
+    state_bytes = (16 if prec == "c128" else 8) << n
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        s.run(arr)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        info = s.info()
+        launches_per_step = info["last_launches"]
+        passes = info["last_passes"]
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(local_rank)
+        clk.start()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (not inside the events)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        clocks = clk.stop()
+    per = [a.elapsed_time(b) for a, b in ev]  # ms
+    t_total = sum(per)
+    if world > 1:
+        t = torch.tensor([t_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total = float(t.item())
+    ms_per_step = t_total / args.steps
+    value = world * args.steps / (t_total / 1e3)
+
+    # ---- e2e: pinned host state in, circuit, full state out, every step
+    h_in = torch.empty(state_bytes, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(state_bytes, dtype=torch.uint8, pin_memory=True)
+    s.read_ptr(h_in.data_ptr(), 1 << n)  # a valid state to start from
+    e2e_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    e_ev = []
+    for i in range(e2e_steps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s.write_ptr(h_in.data_ptr(), 1 << n)
+        s.run(arr)
+        s.read_ptr(h_out.data_ptr(), 1 << n)
+        b.record(stream)
+        if i > 0:
+            e_ev.append((a, b))
+    torch.cuda.synchronize()
+    e_ms = sum(a.elapsed_time(b) for a, b in e_ev) / len(e_ev)
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+
+    peak, peak_kind = load_peaks()
+    # dominant kernel = fused_pass_kernel (every launch of the step is one);
+    # algorithmic bytes per launch = read + write of the whole state (2*Ns).
+    avg_launch_ms = ms_per_step / max(launches_per_step, 1)
+    achieved = 2 * state_bytes / (avg_launch_ms / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "circuit/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if prec == "c128" else "f32", "data": "synthetic",
+        "config": {"workload": desc, "circuit": fam, "qubits": n, "trotter_steps": steps_c or None,
+                   "gates": len(ops), "precision": prec, "state_bytes": state_bytes,
+                   "initial_state": "splitmix64 seed 12345 (DESIGN input recipe)",
+                   "l2": "flushed (512 MiB write) between timed iterations",
+                   "parallelism": f"replicas x{world}", "fused_passes_per_step": passes,
+                   "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"]},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "roofline": {"bound": "hbm", "kernel": "fused_pass_kernel", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "traffic": None,
+                     "bytes_per_launch": 2 * state_bytes,
+                     "avg_launch_ms": avg_launch_ms},
+        "e2e": {"value": world / (e_ms / 1e3), "unit": "circuit/s", "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes, "ms_per_step": e_ms},
+        "clocks": clocks,
+    }
+    s.close()
+    return out
+
+
+def sweep(args, local_rank):
+    """Extra single-GPU measurements reported beside the main line: per-gate
+    HBM GB/s at n=30 and fused-pass GB/s for QFT-30 (HBM regime)."""
+    import torch
+    import paper_2303_00123_b200 as qc
+    import qcgen
+    res = {}
+    peak, _ = load_peaks()
+    for prec in ("c128", "c64"):
+        n = 30
+        sb = (16 if prec == "c128" else 8) << n
+        s = qc.State(n, prec, device=local_rank)
+        stream = torch.cuda.ExternalStream(s.stream)
+        s.init_random(1)
+        ops = qcgen.qft(n)
+        arr = qc.encode_ops(ops)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                s.run(arr)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 3
+            a.record(stream)
+            for _ in range(reps):
+                s.run(arr)
+            b.record(stream)
+            torch.cuda.synchronize()
+        t = a.elapsed_time(b) / reps
+        passes = s.info()["last_passes"]
+        gbps = 2 * sb * passes / (t / 1e3) / 1e9
+        res[f"qft30_{prec}"] = {"ms": t, "passes": passes, "fused_pass_GBps": gbps,
+                                "frac_of_measured_hbm": gbps / peak}
+        # per-gate (unfused) GB/s for a few gate classes and qubit positions
+        s.set_option("fusion", 0)
+        s.set_option("relabel_swap", 0)
+        pg = {}
+        for name, qs, arg, nbytes in (("H", (0,), None, 2 * sb), ("H", (15,), None, 2 * sb),
+                                      ("H", (29,), None, 2 * sb), ("RZ", (12,), 0.3, 2 * sb),
+                                      ("P", (12,), 0.3, sb), ("X", (3,), None, 2 * sb),
+                                      ("CNOT", (4, 20), None, sb), ("CP", (2, 27), 0.2, sb // 2),
+                                      ("SWAP", (1, 28), None, sb), ("U2", (7, 22), "U", 2 * sb)):
+            g = qcgen.Op(name, qs, theta=arg if isinstance(arg, float) else None,
+                         matrix=qcgen.random_unitary(4, np.random.default_rng(0)) if arg == "U" else None)
+            ga = qc.encode_ops([g])
+            with torch.cuda.stream(stream):
+                s.run(ga)
+                torch.cuda.synchronize()
+                a.record(stream)
+                for _ in range(5):
+                    s.run(ga)
+                b.record(stream)
+                torch.cuda.synchronize()
+            tg = a.elapsed_time(b) / 5
+            pg[f"{name}{list(qs)}"] = {"ms": round(tg, 4), "GBps": round(nbytes / (tg / 1e3) / 1e9, 1)}
+        res[f"per_gate_n30_{prec}"] = pg
+        s.close()
+        torch.cuda.empty_cache()
+    return res
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (deliberately slow CPU program) as it stands."""
+    if rank != 0:
+        return None
+    fam, n, steps_c, prec, desc = CONFIGS[args.config]
+    rate, cores, sample = cpu_oracle_rate(args.config, budget_s=max(5.0, 4.0 * args.steps))
+    return {"impl": "reference", "metric": METRIC, "value": rate, "unit": "circuit/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "circuit": fam, "qubits": n, "precision": prec},
+            "cpu_baseline": {"value": rate, "unit": "circuit/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": rate, "unit": "circuit/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="tfxy20", choices=sorted(CONFIGS))
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1:
+        if not args.no_sweep:
+            out["sweep"] = sweep(args, local_rank)
+        if not args.no_cpu:
+            rate, cores, sample = cpu_oracle_rate(args.config)
+            out["cpu_baseline"] = {"value": rate, "unit": "circuit/s", "cores": cores,
+                                   "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

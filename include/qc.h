@@ -1,0 +1,202 @@
+/*
+ * qc.h -- C ABI of the B200-native state-vector gate engine (libqc.so).
+ *
+ * The library applies a quantum circuit's 1- and 2-qubit gates to a
+ * 2^n-amplitude complex state vector resident in B200 HBM.  It implements the
+ * hot path of qclab++ (arXiv 2303.00123).  Citations "P:n" are PAPER.md lines.
+ *
+ * Semantics fixed by the paper:
+ *   - Each gate is psi = (I_l (x) U (x) I_r) phi            eq:kron.
+ *   - Qubit numbering is Definition 1: qubit 0 is the MOST
+ *     significant bit of the amplitude index; qubit q is bit n-1-q.
+ *   - 1-qubit gates = 2^{n-1} independent 2x2 matvecs (Alg. alg:1q);
+ *     controlled 1-qubit gates update the control-selected half (Alg.
+ *     alg:ctrl-1q, all four control cases); 2-qubit gates are
+ *     2^{n-2} 4x4 matvecs on any (non-contiguous) qubit pair (Alg. alg:2q,
+ *     P:883-919); SWAP and CNOT are pure element moves (P:852-854,
+ *     P:921-938); a doubly controlled gate touches a quarter.
+ *   - A circuit is the ordered product of its gates.
+ *   Matrix conventions the paper leaves open are DESIGN.md readings R1-R14
+ *   (R1: the 4x4 of a 2-qubit gate is indexed big-endian over the LISTED
+ *   qubit order, i.e. eq:kron, not Alg. alg:2q read literally; R4: gate
+ *   matrices; R11: X/CNOT/SWAP/CCX are bit-exact moves).
+ *
+ * Data layout: the state is one device buffer of 2^n interleaved complex
+ * numbers (QC_COMPLEX64: 2 x float, 8 B; QC_COMPLEX128: 2 x double, 16 B).
+ * The library may keep the amplitudes in a PERMUTED bit order (SWAP gates are
+ * applied as relabels when QC_OPT_RELABEL_SWAP is on); qc_state_read /
+ * qc_state_write always speak canonical (Definition 1) order.
+ *
+ * Ownership: the state owns its device memory (qc_state_create*), except for
+ * qc_state_wrap, where the caller keeps ownership and guarantees lifetime.
+ * Every host pointer argument is borrowed for the duration of the call only.
+ *
+ * Errors: every call returns a qc_status; qc_last_error() returns a
+ * thread-local message for the last failing call on this thread.  Argument
+ * validation happens BEFORE any device work, so on QC_ERR_INVALID_ARG the
+ * state is unchanged (qc_run_circuit validates the whole list first).
+ * Asynchronous CUDA failures surface at the next call that checks the stream
+ * and mark the state failed: every later call returns QC_ERR_STATE_FAILED.
+ *
+ * Threading: a qc_state is not thread-safe; distinct states are independent.
+ * apply/run enqueue on the state's CUDA stream and return; read, norm2 and
+ * sync block until the stream is drained.
+ */
+#ifndef QC_H_
+#define QC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QC_ABI_VERSION 1
+
+typedef enum {
+    QC_OK = 0,
+    QC_ERR_INVALID_ARG = 1,   /* bad n, qubit out of range / repeated, NULL, NaN theta, range */
+    QC_ERR_OUT_OF_MEMORY = 2, /* device allocation failed (message states s*2^n bytes) */
+    QC_ERR_CUDA = 3,          /* a CUDA runtime call failed */
+    QC_ERR_NCCL = 4,          /* reserved for the sharded layer */
+    QC_ERR_UNSUPPORTED = 5,   /* valid request this build does not implement */
+    QC_ERR_STATE_FAILED = 6   /* an earlier asynchronous failure poisoned the state */
+} qc_status;
+
+typedef enum {
+    QC_COMPLEX64 = 0,   /* interleaved 2 x float32 per amplitude (8 B)  */
+    QC_COMPLEX128 = 1   /* interleaved 2 x float64 per amplitude (16 B) */
+} qc_precision;
+
+/* Gate kinds.  "qubits" lists controls first.  Matrices:
+ *   H = [[1,1],[1,-1]]/sqrt2;  X, Y, Z per P:617-631;  P(t) = diag(1, e^{it});
+ *   RX(t) = exp(-i t X/2), RY(t) = exp(-i t Y/2), RZ(t) = diag(e^{-it/2}, e^{it/2});
+ *   CNOT/CZ/CP/CU1: 1 control + target;  CCX: 2 controls + target (Toffoli);
+ *   SWAP: P:921-930;  U1: any 2x2;  U2: any 4x4 on (qubits[0], qubits[1]),
+ *   row/column index = 2*bit(qubits[0]) + bit(qubits[1]) (eq:kron, R1).     */
+typedef enum {
+    QC_H = 0, QC_X = 1, QC_Y = 2, QC_Z = 3, QC_P = 4, QC_RX = 5, QC_RY = 6, QC_RZ = 7,
+    QC_CNOT = 8, QC_CZ = 9, QC_CP = 10, QC_SWAP = 11,
+    QC_U1 = 12, QC_CU1 = 13, QC_U2 = 14, QC_CCX = 15
+} qc_op;
+
+#define QC_CTRL_ONES 0xFFFFFFFFu  /* default: every control must be |1> */
+
+/* One gate of an op list (288 bytes, 8-byte aligned). */
+typedef struct qc_gate {
+    int32_t op;          /* qc_op                                                    */
+    int32_t qubits[3];   /* listed qubits (controls first); entries past arity ignored */
+    uint32_t ctrl_state; /* bit t = required state of listed control t (low nctrl bits) */
+    uint32_t flags;      /* reserved, must be 0                                      */
+    double theta;        /* P, RX, RY, RZ, CP (finite); ignored otherwise            */
+    double m[32];        /* U1/CU1: 2x2, U2: 4x4; interleaved re,im; row-major       */
+} qc_gate;
+
+typedef struct qc_state qc_state;  /* opaque handle */
+
+typedef enum {
+    QC_OPT_FUSION = 0,        /* 1 (default): fused tile passes; 0: one kernel per gate    */
+    QC_OPT_RELABEL_SWAP = 1,  /* 1 (default): SWAP = relabel (0 bytes moved); 0: data move  */
+    QC_OPT_USE_GRAPH = 2,     /* 1 (default): replay repeated circuits as CUDA graphs       */
+    QC_OPT_TILE_BITS = 3,     /* 0 (default): auto (64 KiB tiles); else 4..13               */
+    QC_OPT_CTAS = 4           /* 0 (default): one CTA per SM; else grid size of fused passes */
+} qc_option;
+
+/* Counters of the most recent qc_run_circuit / qc_apply_gate. */
+typedef struct qc_info {
+    int32_t n;
+    int32_t precision;        /* qc_precision */
+    void* device_ptr;         /* amplitudes (physical order, see layout)        */
+    void* stream;             /* cudaStream_t the state enqueues on             */
+    int32_t layout[64];       /* layout[q] = physical bit position of qubit q   */
+    int32_t layout_is_canonical;
+    int64_t last_gates;       /* gates in the last run                          */
+    int64_t last_passes;      /* fused tile passes (or per-gate kernels)        */
+    int64_t last_launches;    /* kernels launched by the last run               */
+    int64_t last_relabels;    /* SWAPs applied as relabels                      */
+    int32_t last_graph;       /* 1 if the last run replayed a CUDA graph        */
+    int32_t tile_bits;        /* k of the last fused run                        */
+} qc_info;
+
+/* ---------------------------------------------------------------- lifetime */
+
+/* Allocate an n-qubit state on the current CUDA device, initialised to |0...0>,
+ * with its own non-blocking stream.  1 <= n <= 40.  Returns NULL on error
+ * (qc_last_error() says why; out of memory names the s*2^n byte count). */
+qc_state* qc_state_create(int n, qc_precision p);
+
+/* As qc_state_create, on `device`, enqueuing on `cuda_stream` (a cudaStream_t;
+ * NULL = the library creates a non-blocking stream). */
+qc_status qc_state_create_ex(int n, qc_precision p, int device, void* cuda_stream,
+                             qc_state** out);
+
+/* Borrow caller-owned device memory of s*2^n bytes (e.g. a torch tensor) and a
+ * stream.  Contents are taken as the state in canonical order. */
+qc_status qc_state_wrap(int n, qc_precision p, void* dev_ptr, void* cuda_stream,
+                        qc_state** out);
+
+/* Synchronise the stream and free everything the state owns.  NULL is a no-op. */
+void qc_state_destroy(qc_state* s);
+
+/* ------------------------------------------------------------ initial data */
+
+/* |k>, canonical index k < 2^n.  Resets the layout to canonical. */
+qc_status qc_state_init_basis(qc_state* s, uint64_t k);
+
+/* The seeded random state of DESIGN.md's input recipe, generated on device:
+ *   re_i = u(sm(seed,2i))*c, im_i = u(sm(seed,2i+1))*c, c = sqrt(1.5/2^n),
+ *   sm = counter-based splitmix64, u(x) = (x>>11)*2^-52 - 1;
+ * complex64 rounds each double to float.  Resets the layout to canonical. */
+qc_status qc_state_init_random(qc_state* s, uint64_t seed);
+
+/* --------------------------------------------------------------- the path */
+
+/* Apply one gate with its own per-gate kernel (no fusion).  `qubits` holds
+ * arity(op) distinct qubits in [0,n), controls first (controls = |1>).
+ * `matrix`: NULL for H X Y Z CNOT CZ SWAP CCX; one double theta for P RX RY RZ
+ * CP; 8 doubles (2x2) for U1 and CU1; 32 doubles (4x4) for U2, interleaved
+ * re,im, row-major.  Enqueued; returns without waiting. */
+qc_status qc_apply_gate(qc_state* s, qc_op op, const int* qubits, const double* matrix);
+
+/* Apply n_ops gates in order (Alg. 1-3 semantics, eq:kron product).  The
+ * whole list is validated first (all-or-nothing).  With QC_OPT_FUSION the
+ * planner groups gates into fused tile passes (one HBM round trip each);
+ * otherwise one kernel per gate.  Enqueued; returns without waiting. */
+qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops);
+
+/* ------------------------------------------------------------------ I/O */
+
+/* Copy canonical amplitudes [first, first+count) to host memory (count*s
+ * bytes).  Blocks.  Undoes any pending relabel on the fly (gather kernel). */
+qc_status qc_state_read(qc_state* s, uint64_t first, uint64_t count, void* host_dst);
+
+/* Write canonical amplitudes [first, first+count) from host memory.  Blocks
+ * until the copy has been consumed.  Leaves the layout unchanged. */
+qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void* host_src);
+
+/* Permute the amplitudes back to canonical order in place (no-op if already). */
+qc_status qc_state_canonicalize(qc_state* s);
+
+/* Block until all enqueued work on the state's stream is done; report any
+ * asynchronous CUDA failure. */
+qc_status qc_state_sync(qc_state* s);
+
+/* sum_i |psi_i|^2 in double (device reduction).  Blocks. */
+qc_status qc_state_norm2(qc_state* s, double* out);
+
+/* ---------------------------------------------------------- configuration */
+
+qc_status qc_set_option(qc_state* s, qc_option opt, int64_t value);
+qc_status qc_get_info(const qc_state* s, qc_info* out);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* qc_last_error(void);
+
+/* Library version string ("qc-b200 <abi> sm_100a"). */
+const char* qc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QC_H_ */

@@ -1,0 +1,654 @@
+// api.cu -- the C ABI of include/qc.h: validation, lowering, planning,
+// launching, I/O.  Host code only (kernels live in kernels_*.cu).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "qc_internal.h"
+
+using namespace qc;
+
+namespace {
+
+thread_local std::string g_err;
+
+qc_status fail(qc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+const int kArity[16] = {1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 1, 2, 2, 3};
+const int kNctrl[16] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 0, 2};
+const char* kName[16] = {"H", "X", "Y", "Z", "P", "RX", "RY", "RZ",
+                         "CNOT", "CZ", "CP", "SWAP", "U1", "CU1", "U2", "CCX"};
+
+struct PlanEntry {
+  std::vector<qc_gate> ops;          // exact copy (collision check)
+  std::vector<int> layout_in, layout_out;
+  std::vector<PassDesc> passes;
+  void* d_subs = nullptr;
+  void* d_ops = nullptr;
+  int64_t relabels = 0;
+  int uses = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int ctas = 0;
+  int tile_bits = 0;
+  ~PlanEntry() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (d_subs) cudaFree(d_subs);
+    if (d_ops) cudaFree(d_ops);
+  }
+};
+
+}  // namespace
+
+struct qc_state {
+  int n = 0;
+  qc_precision prec = QC_COMPLEX128;
+  bool dbl = true;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* d = nullptr;
+  bool own_mem = false;
+  size_t bytes = 0;
+  int layout[64];
+  bool failed = false;
+  // options
+  int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0;
+  // stats
+  int64_t last_gates = 0, last_passes = 0, last_launches = 0, last_relabels = 0;
+  int last_graph = 0, last_k = 0;
+  // plan cache
+  std::unordered_map<uint64_t, std::unique_ptr<PlanEntry>> plans;
+  cudaStream_t cap_stream = nullptr;
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  double* d_partial = nullptr;
+};
+
+namespace {
+
+size_t amp_bytes(const qc_state* s) { return s->dbl ? 16 : 8; }
+
+void canonical_layout(qc_state* s) {
+  for (int q = 0; q < s->n; ++q) s->layout[q] = s->n - 1 - q;
+}
+bool layout_is_canonical(const qc_state* s) {
+  for (int q = 0; q < s->n; ++q)
+    if (s->layout[q] != s->n - 1 - q) return false;
+  return true;
+}
+
+qc_status check_state(qc_state* s) {
+  if (!s) return fail(QC_ERR_INVALID_ARG, "state is NULL");
+  if (s->failed) return fail(QC_ERR_STATE_FAILED, "state failed earlier (asynchronous CUDA error)");
+  cudaError_t e = cudaSetDevice(s->device);
+  if (e != cudaSuccess) return fail(QC_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return QC_OK;
+}
+
+qc_status cuda_fail(qc_state* s, int e, const char* what) {
+  if (s) s->failed = true;
+  return fail(QC_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)e));
+}
+
+qc_status validate_gate(int n, const qc_gate& g, size_t idx) {
+  if (g.op < 0 || g.op > 15) return fail(QC_ERR_INVALID_ARG, "op %zu: unknown op code %d", idx, g.op);
+  if (g.flags != 0) return fail(QC_ERR_INVALID_ARG, "op %zu: flags must be 0", idx);
+  const int k = kArity[g.op];
+  for (int t = 0; t < k; ++t) {
+    if (g.qubits[t] < 0 || g.qubits[t] >= n)
+      return fail(QC_ERR_INVALID_ARG, "op %zu (%s): qubit %d out of range [0,%d)", idx, kName[g.op],
+                  g.qubits[t], n);
+    for (int u = 0; u < t; ++u)
+      if (g.qubits[u] == g.qubits[t])
+        return fail(QC_ERR_INVALID_ARG, "op %zu (%s): qubit %d repeated", idx, kName[g.op], g.qubits[t]);
+  }
+  const bool has_theta = g.op == QC_P || g.op == QC_RX || g.op == QC_RY || g.op == QC_RZ || g.op == QC_CP;
+  if (has_theta && !std::isfinite(g.theta))
+    return fail(QC_ERR_INVALID_ARG, "op %zu (%s): theta is not finite", idx, kName[g.op]);
+  const int nm = g.op == QC_U2 ? 32 : ((g.op == QC_U1 || g.op == QC_CU1) ? 8 : 0);
+  for (int i = 0; i < nm; ++i)
+    if (!std::isfinite(g.m[i]))
+      return fail(QC_ERR_INVALID_ARG, "op %zu (%s): matrix entry %d not finite", idx, kName[g.op], i);
+  return QC_OK;
+}
+
+// Lower one validated gate to a physical-bit kernel class (DESIGN R4 matrices).
+PGate lower(const qc_gate& g, const int* layout) {
+  PGate p;
+  const int nc = kNctrl[g.op];
+  for (int t = 0; t < nc; ++t) {
+    const int b = layout[g.qubits[t]];
+    p.cmask |= 1ull << b;
+    if ((g.ctrl_state >> t) & 1u) p.cval |= 1ull << b;
+  }
+  const int tq = g.qubits[nc];
+  p.t0 = layout[tq];
+  const double th = g.theta;
+  const double c = std::cos(th / 2), s = std::sin(th / 2);
+  const double h = 1.0 / std::sqrt(2.0);
+  const cd I(0, 1);
+  auto dense = [&](cd a, cd b, cd cc, cd d) {
+    p.kind = GK::DENSE1;
+    p.m[0] = a; p.m[1] = b; p.m[2] = cc; p.m[3] = d;
+  };
+  auto diag = [&](cd d0, cd d1, bool one) {
+    p.kind = GK::DIAG1;
+    p.m[0] = d0; p.m[1] = d1;
+    p.d0_is_one = one;
+  };
+  switch (g.op) {
+    case QC_H: dense(h, h, h, -h); break;
+    case QC_X: case QC_CNOT: case QC_CCX: p.kind = GK::PERM1; break;
+    case QC_Y: dense(0, -I, I, 0); break;
+    case QC_Z: case QC_CZ: diag(1.0, -1.0, true); break;
+    case QC_P: case QC_CP: diag(1.0, std::exp(I * th), true); break;
+    case QC_RX: dense(c, -I * s, -I * s, c); break;
+    case QC_RY: dense(c, -s, s, c); break;
+    case QC_RZ: diag(std::exp(-I * (th / 2)), std::exp(I * (th / 2)), false); break;
+    case QC_U1: case QC_CU1:
+      dense(cd(g.m[0], g.m[1]), cd(g.m[2], g.m[3]), cd(g.m[4], g.m[5]), cd(g.m[6], g.m[7]));
+      break;
+    case QC_SWAP:
+      p.kind = GK::SWAP2;
+      p.t0 = layout[g.qubits[0]];
+      p.t1 = layout[g.qubits[1]];
+      break;
+    case QC_U2:
+      p.kind = GK::DENSE2;
+      p.t0 = layout[g.qubits[0]];
+      p.t1 = layout[g.qubits[1]];
+      for (int i = 0; i < 16; ++i) p.m[i] = cd(g.m[2 * i], g.m[2 * i + 1]);
+      break;
+  }
+  return p;
+}
+
+uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt) {
+  uint64_t h = 0xcbf29ce484222325ull ^ salt;
+  auto mix = [&](uint64_t w) {
+    h ^= w;
+    h *= 0x100000001b3ull;
+    h ^= h >> 29;
+  };
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(ops);
+  const size_t nw = n * sizeof(qc_gate) / 8;
+  for (size_t i = 0; i < nw; ++i) mix(w[i]);
+  for (int q = 0; q < nq; ++q) mix((uint64_t)layout[q] + 977ull * q);
+  mix(n);
+  return h;
+}
+
+template <typename T>
+void to_prec(const FOpT<double>& a, FOpT<T>& b) {
+  std::memcpy(&b, &a, offsetof(FOpT<double>, m));
+  for (int i = 0; i < 32; ++i) b.m[i] = (T)a.m[i];
+}
+
+// Build (or fetch) the fused plan for this op list and the current layout.
+qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
+  const int n = s->n;
+  int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
+  if (k > n) k = n;
+  int rb = s->dbl ? 5 : 6;
+  if (rb > k - 2) rb = k - 2;
+  if (rb < 1) rb = 1;
+  const int ctas = s->ctas ? s->ctas : sm_count();
+  const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
+                        ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
+  const uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
+  auto it = s->plans.find(key);
+  if (it != s->plans.end()) {
+    PlanEntry* e = it->second.get();
+    if (e->ops.size() == n_ops && std::memcmp(e->ops.data(), ops, n_ops * sizeof(qc_gate)) == 0 &&
+        std::memcmp(e->layout_in.data(), s->layout, n * sizeof(int)) == 0) {
+      *out = e;
+      return QC_OK;
+    }
+  }
+  auto e = std::make_unique<PlanEntry>();
+  e->ops.assign(ops, ops + n_ops);
+  e->layout_in.assign(s->layout, s->layout + n);
+  e->ctas = ctas;
+  e->tile_bits = k;
+  // lower in order, applying SWAP relabels to a running layout
+  int lay[64];
+  std::memcpy(lay, s->layout, sizeof(int) * n);
+  std::vector<PGate> gates;
+  gates.reserve(n_ops);
+  for (size_t i = 0; i < n_ops; ++i) {
+    if (ops[i].op == QC_SWAP && s->relabel) {
+      std::swap(lay[ops[i].qubits[0]], lay[ops[i].qubits[1]]);
+      e->relabels++;
+      continue;
+    }
+    PGate g = lower(ops[i], lay);
+    g.src_op = (int)i;
+    gates.push_back(g);
+  }
+  e->layout_out.assign(lay, lay + n);
+  if (!gates.empty()) {
+    FusedPlan fp = plan_fused(n, k, rb, gates);
+    if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
+    for (auto& p : fp.passes) e->passes.push_back(p.desc);
+    const size_t sb = fp.subs.size() * sizeof(SubStageDesc);
+    cudaError_t ce = cudaMalloc(&e->d_subs, sb);
+    if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
+    ce = cudaMemcpy(e->d_subs, fp.subs.data(), sb, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
+    if (s->dbl) {
+      const size_t ob = fp.ops.size() * sizeof(FOpT<double>);
+      ce = cudaMalloc(&e->d_ops, ob);
+      if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
+      ce = cudaMemcpy(e->d_ops, fp.ops.data(), ob, cudaMemcpyHostToDevice);
+    } else {
+      std::vector<FOpT<float>> f(fp.ops.size());
+      for (size_t i = 0; i < f.size(); ++i) to_prec(fp.ops[i], f[i]);
+      const size_t ob = f.size() * sizeof(FOpT<float>);
+      ce = cudaMalloc(&e->d_ops, ob);
+      if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
+      ce = cudaMemcpy(e->d_ops, f.data(), ob, cudaMemcpyHostToDevice);
+    }
+    if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
+  }
+  PlanEntry* raw = e.get();
+  if (s->plans.size() > 64) s->plans.clear();
+  s->plans[key] = std::move(e);
+  *out = raw;
+  return QC_OK;
+}
+
+int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) {
+  for (const PassDesc& pd : e->passes) {
+    const int r = launch_fused_pass(s->d, s->dbl, pd, e->d_subs, e->d_ops, e->ctas, st);
+    if (r) return r;
+  }
+  return 0;
+}
+
+qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  static bool configured[2] = {false, false};
+  if (!configured[s->dbl]) {
+    const int r = fused_configure(s->dbl, 0);
+    if (r) return cuda_fail(s, r, "cudaFuncSetAttribute(fused)");
+    configured[s->dbl] = true;
+  }
+  PlanEntry* e = nullptr;
+  qc_status st = get_plan(s, ops, n_ops, &e);
+  if (st != QC_OK) return st;
+  e->uses++;
+  s->last_graph = 0;
+  int r = 0;
+  if (s->use_graph && e->uses >= 2 && !e->passes.empty()) {
+    if (!e->exec) {
+      if (!s->cap_stream) {
+        r = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
+        if (r) return cuda_fail(s, r, "cudaStreamCreate");
+      }
+      r = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+      if (r) return cuda_fail(s, r, "cudaStreamBeginCapture");
+      const int rl = enqueue_plan(s, e, s->cap_stream);
+      r = cudaStreamEndCapture(s->cap_stream, &e->graph);
+      if (rl) return cuda_fail(s, rl, "fused launch (capture)");
+      if (r) return cuda_fail(s, r, "cudaStreamEndCapture");
+      r = cudaGraphInstantiate(&e->exec, e->graph, 0);
+      if (r) return cuda_fail(s, r, "cudaGraphInstantiate");
+    }
+    r = cudaGraphLaunch(e->exec, s->stream);
+    if (r) return cuda_fail(s, r, "cudaGraphLaunch");
+    s->last_graph = 1;
+  } else {
+    r = enqueue_plan(s, e, s->stream);
+    if (r) return cuda_fail(s, r, "fused pass launch");
+  }
+  std::memcpy(s->layout, e->layout_out.data(), sizeof(int) * s->n);
+  s->last_passes = (int64_t)e->passes.size();
+  s->last_launches = (int64_t)e->passes.size();
+  s->last_relabels = e->relabels;
+  s->last_k = e->tile_bits;
+  return QC_OK;
+}
+
+qc_status run_unfused(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  int64_t launches = 0, relabels = 0;
+  for (size_t i = 0; i < n_ops; ++i) {
+    if (ops[i].op == QC_SWAP && s->relabel) {
+      std::swap(s->layout[ops[i].qubits[0]], s->layout[ops[i].qubits[1]]);
+      ++relabels;
+      continue;
+    }
+    const PGate g = lower(ops[i], s->layout);
+    const int r = launch_gate(s->d, s->n, s->dbl, g, s->stream);
+    if (r) return cuda_fail(s, r, "gate kernel launch");
+    ++launches;
+  }
+  s->last_passes = launches;
+  s->last_launches = launches;
+  s->last_relabels = relabels;
+  s->last_graph = 0;
+  s->last_k = 0;
+  return QC_OK;
+}
+
+qc_status ensure_stage(qc_state* s, size_t bytes) {
+  if (s->stage_bytes >= bytes) return QC_OK;
+  if (s->d_stage) cudaFree(s->d_stage);
+  s->d_stage = nullptr;
+  s->stage_bytes = 0;
+  cudaError_t e = cudaMalloc(&s->d_stage, bytes);
+  if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "staging buffer of %zu B: %s", bytes,
+                                    cudaGetErrorString(e));
+  s->stage_bytes = bytes;
+  return QC_OK;
+}
+
+qc_status new_state(int n, qc_precision p, int device, void* stream, void* dev_ptr, qc_state** out) {
+  if (!out) return fail(QC_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > kMaxQubits) return fail(QC_ERR_INVALID_ARG, "n=%d outside [1,%d]", n, kMaxQubits);
+  if (p != QC_COMPLEX64 && p != QC_COMPLEX128) return fail(QC_ERR_INVALID_ARG, "bad precision %d", (int)p);
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return fail(QC_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(QC_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  auto s = std::make_unique<qc_state>();
+  s->n = n;
+  s->prec = p;
+  s->dbl = (p == QC_COMPLEX128);
+  s->device = device;
+  s->bytes = (size_t)(s->dbl ? 16 : 8) << n;
+  canonical_layout(s.get());
+  if (stream) {
+    s->stream = reinterpret_cast<cudaStream_t>(stream);
+  } else {
+    e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(QC_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    s->own_stream = true;
+  }
+  if (dev_ptr) {
+    if (reinterpret_cast<uintptr_t>(dev_ptr) % 16)
+      return fail(QC_ERR_INVALID_ARG, "wrapped device pointer must be 16-byte aligned");
+    s->d = dev_ptr;
+  } else {
+    e = cudaMalloc(&s->d, s->bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (s->own_stream) cudaStreamDestroy(s->stream);
+      return fail(QC_ERR_OUT_OF_MEMORY, "cannot allocate the %d-qubit state: %zu bytes (%s)", n, s->bytes,
+                  cudaGetErrorString(e));
+    }
+    s->own_mem = true;
+    const int r = launch_init_basis(s->d, n, s->dbl, 0, s->stream);
+    if (r) {
+      cudaFree(s->d);
+      if (s->own_stream) cudaStreamDestroy(s->stream);
+      return fail(QC_ERR_CUDA, "init: %s", cudaGetErrorString((cudaError_t)r));
+    }
+  }
+  *out = s.release();
+  return QC_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* qc_last_error(void) { return g_err.c_str(); }
+
+const char* qc_version(void) { return "qc-b200 1 sm_100a"; }
+
+qc_state* qc_state_create(int n, qc_precision p) {
+  qc_state* s = nullptr;
+  if (new_state(n, p, -1, nullptr, nullptr, &s) != QC_OK) return nullptr;
+  return s;
+}
+
+qc_status qc_state_create_ex(int n, qc_precision p, int device, void* cuda_stream, qc_state** out) {
+  if (device < 0) return fail(QC_ERR_INVALID_ARG, "device must be >= 0");
+  return new_state(n, p, device, cuda_stream, nullptr, out);
+}
+
+qc_status qc_state_wrap(int n, qc_precision p, void* dev_ptr, void* cuda_stream, qc_state** out) {
+  if (!dev_ptr) return fail(QC_ERR_INVALID_ARG, "dev_ptr is NULL");
+  return new_state(n, p, -1, cuda_stream, dev_ptr, out);
+}
+
+void qc_state_destroy(qc_state* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  s->plans.clear();
+  if (s->own_mem && s->d) cudaFree(s->d);
+  if (s->d_stage) cudaFree(s->d_stage);
+  if (s->d_partial) cudaFree(s->d_partial);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->own_stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+qc_status qc_state_init_basis(qc_state* s, uint64_t k) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if (k >> s->n) return fail(QC_ERR_INVALID_ARG, "basis index %llu >= 2^%d", (unsigned long long)k, s->n);
+  canonical_layout(s);
+  const int r = launch_init_basis(s->d, s->n, s->dbl, k, s->stream);
+  if (r) return cuda_fail(s, r, "init_basis");
+  return QC_OK;
+}
+
+qc_status qc_state_init_random(qc_state* s, uint64_t seed) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  canonical_layout(s);
+  const int r = launch_init_random(s->d, s->n, s->dbl, seed, s->stream);
+  if (r) return cuda_fail(s, r, "init_random");
+  return QC_OK;
+}
+
+qc_status qc_apply_gate(qc_state* s, qc_op op, const int* qubits, const double* matrix) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if ((int)op < 0 || (int)op > 15) return fail(QC_ERR_INVALID_ARG, "unknown op code %d", (int)op);
+  if (!qubits) return fail(QC_ERR_INVALID_ARG, "qubits is NULL");
+  qc_gate g;
+  std::memset(&g, 0, sizeof g);
+  g.op = op;
+  for (int t = 0; t < kArity[op]; ++t) g.qubits[t] = qubits[t];
+  g.ctrl_state = QC_CTRL_ONES;
+  const bool has_theta = op == QC_P || op == QC_RX || op == QC_RY || op == QC_RZ || op == QC_CP;
+  const int nm = op == QC_U2 ? 32 : ((op == QC_U1 || op == QC_CU1) ? 8 : 0);
+  if ((has_theta || nm) && !matrix) return fail(QC_ERR_INVALID_ARG, "%s needs a matrix/theta argument", kName[op]);
+  if (has_theta) g.theta = matrix[0];
+  for (int i = 0; i < nm; ++i) g.m[i] = matrix[i];
+  st = validate_gate(s->n, g, 0);
+  if (st != QC_OK) return st;
+  return run_unfused(s, &g, 1);
+}
+
+qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if (n_ops && !ops) return fail(QC_ERR_INVALID_ARG, "ops is NULL");
+  for (size_t i = 0; i < n_ops; ++i) {
+    st = validate_gate(s->n, ops[i], i);
+    if (st != QC_OK) return st;
+  }
+  s->last_gates = (int64_t)n_ops;
+  if (n_ops == 0) {
+    s->last_passes = s->last_launches = s->last_relabels = 0;
+    return QC_OK;
+  }
+  if (s->fusion && s->n >= kSlotBits) return run_fused(s, ops, n_ops);
+  return run_unfused(s, ops, n_ops);
+}
+
+qc_status qc_state_sync(qc_state* s) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  return QC_OK;
+}
+
+qc_status qc_state_read(qc_state* s, uint64_t first, uint64_t count, void* host_dst) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  const uint64_t N = 1ull << s->n;
+  if (!host_dst && count) return fail(QC_ERR_INVALID_ARG, "host_dst is NULL");
+  if (first > N || count > N - first)
+    return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
+                (unsigned long long)count, s->n);
+  if (!count) return QC_OK;
+  const size_t ab = amp_bytes(s);
+  cudaError_t e;
+  if (layout_is_canonical(s)) {
+    e = cudaMemcpyAsync(host_dst, (char*)s->d + first * ab, count * ab, cudaMemcpyDeviceToHost, s->stream);
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemcpyAsync D2H");
+  } else {
+    const uint64_t chunk = std::min<uint64_t>(count, (64ull << 20) / ab);
+    st = ensure_stage(s, chunk * ab);
+    if (st != QC_OK) return st;
+    for (uint64_t c = 0; c < count; c += chunk) {
+      const uint64_t m = std::min<uint64_t>(chunk, count - c);
+      const int r = launch_gather(s->d, s->d_stage, s->n, s->dbl, s->layout, first + c, m, false, s->stream);
+      if (r) return cuda_fail(s, r, "gather");
+      e = cudaMemcpyAsync((char*)host_dst + c * ab, s->d_stage, m * ab, cudaMemcpyDeviceToHost, s->stream);
+      if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemcpyAsync D2H");
+    }
+  }
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  return QC_OK;
+}
+
+qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void* host_src) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  const uint64_t N = 1ull << s->n;
+  if (!host_src && count) return fail(QC_ERR_INVALID_ARG, "host_src is NULL");
+  if (first > N || count > N - first)
+    return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
+                (unsigned long long)count, s->n);
+  if (!count) return QC_OK;
+  const size_t ab = amp_bytes(s);
+  cudaError_t e;
+  if (layout_is_canonical(s)) {
+    e = cudaMemcpyAsync((char*)s->d + first * ab, host_src, count * ab, cudaMemcpyHostToDevice, s->stream);
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemcpyAsync H2D");
+  } else {
+    const uint64_t chunk = std::min<uint64_t>(count, (64ull << 20) / ab);
+    st = ensure_stage(s, chunk * ab);
+    if (st != QC_OK) return st;
+    for (uint64_t c = 0; c < count; c += chunk) {
+      const uint64_t m = std::min<uint64_t>(chunk, count - c);
+      e = cudaMemcpyAsync(s->d_stage, (const char*)host_src + c * ab, m * ab, cudaMemcpyHostToDevice, s->stream);
+      if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemcpyAsync H2D");
+      const int r = launch_gather(s->d, s->d_stage, s->n, s->dbl, s->layout, first + c, m, true, s->stream);
+      if (r) return cuda_fail(s, r, "scatter");
+    }
+  }
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  return QC_OK;
+}
+
+qc_status qc_state_canonicalize(qc_state* s) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  for (int q = 0; q < s->n; ++q) {
+    const int want = s->n - 1 - q;
+    if (s->layout[q] == want) continue;
+    int q2 = -1;
+    for (int u = 0; u < s->n; ++u)
+      if (s->layout[u] == want) q2 = u;
+    PGate g;
+    g.kind = GK::SWAP2;
+    g.t0 = s->layout[q];
+    g.t1 = want;
+    const int r = launch_gate(s->d, s->n, s->dbl, g, s->stream);
+    if (r) return cuda_fail(s, r, "canonicalize");
+    s->layout[q2] = s->layout[q];
+    s->layout[q] = want;
+  }
+  return QC_OK;
+}
+
+qc_status qc_state_norm2(qc_state* s, double* out) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if (!out) return fail(QC_ERR_INVALID_ARG, "out is NULL");
+  const int nb = sm_count() * 4;
+  if (!s->d_partial) {
+    cudaError_t e = cudaMalloc(&s->d_partial, nb * sizeof(double));
+    if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "norm partials: %s", cudaGetErrorString(e));
+  }
+  const int r = launch_norm2(s->d, s->n, s->dbl, s->d_partial, nb, s->stream);
+  if (r) return cuda_fail(s, r, "norm2");
+  std::vector<double> h(nb);
+  cudaError_t e = cudaMemcpyAsync(h.data(), s->d_partial, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemcpyAsync");
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  double t = 0;
+  for (double v : h) t += v;
+  *out = t;
+  return QC_OK;
+}
+
+qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
+  if (!s) return fail(QC_ERR_INVALID_ARG, "state is NULL");
+  switch (opt) {
+    case QC_OPT_FUSION: s->fusion = v != 0; break;
+    case QC_OPT_RELABEL_SWAP: s->relabel = v != 0; break;
+    case QC_OPT_USE_GRAPH: s->use_graph = v != 0; break;
+    case QC_OPT_TILE_BITS:
+      if (v != 0 && (v < 4 || v > 13)) return fail(QC_ERR_INVALID_ARG, "tile bits must be 0 or 4..13");
+      s->tile_bits = (int)v;
+      break;
+    case QC_OPT_CTAS:
+      if (v < 0 || v > 65535) return fail(QC_ERR_INVALID_ARG, "ctas out of range");
+      s->ctas = (int)v;
+      break;
+    default: return fail(QC_ERR_INVALID_ARG, "unknown option %d", (int)opt);
+  }
+  return QC_OK;
+}
+
+qc_status qc_get_info(const qc_state* s, qc_info* out) {
+  if (!s || !out) return fail(QC_ERR_INVALID_ARG, "NULL argument");
+  std::memset(out, 0, sizeof *out);
+  out->n = s->n;
+  out->precision = s->prec;
+  out->device_ptr = s->d;
+  out->stream = s->stream;
+  for (int q = 0; q < s->n; ++q) out->layout[q] = s->layout[q];
+  out->layout_is_canonical = layout_is_canonical(s) ? 1 : 0;
+  out->last_gates = s->last_gates;
+  out->last_passes = s->last_passes;
+  out->last_launches = s->last_launches;
+  out->last_relabels = s->last_relabels;
+  out->last_graph = s->last_graph;
+  out->tile_bits = s->last_k;
+  return QC_OK;
+}
+
+}  // extern "C"

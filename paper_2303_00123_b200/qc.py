@@ -1,0 +1,238 @@
+"""Thin ctypes binding of libqc.so (include/qc.h).  Argument marshalling only:
+every step of the gate path runs in the library's CUDA kernels.  There is no
+CPU fallback -- if the extension is missing this module raises on import of
+the library.
+
+Raw entry points keep the C names (``qc_state_create``, ``qc_apply_gate``,
+``qc_run_circuit``, ``qc_state_read`` ...).  :class:`State` is a small
+convenience wrapper used by the tests and ``bench.py``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqc.so")
+
+QC_OK, QC_ERR_INVALID_ARG, QC_ERR_OUT_OF_MEMORY, QC_ERR_CUDA, QC_ERR_NCCL, \
+    QC_ERR_UNSUPPORTED, QC_ERR_STATE_FAILED = range(7)
+QC_COMPLEX64, QC_COMPLEX128 = 0, 1
+PRECISION = {"c64": QC_COMPLEX64, "c128": QC_COMPLEX128}
+OPS = {"H": 0, "X": 1, "Y": 2, "Z": 3, "P": 4, "RX": 5, "RY": 6, "RZ": 7, "CNOT": 8,
+       "CZ": 9, "CP": 10, "SWAP": 11, "U1": 12, "CU1": 13, "U2": 14, "CCX": 15}
+ARITY = {"H": 1, "X": 1, "Y": 1, "Z": 1, "P": 1, "RX": 1, "RY": 1, "RZ": 1, "CNOT": 2,
+         "CZ": 2, "CP": 2, "SWAP": 2, "U1": 1, "CU1": 2, "U2": 2, "CCX": 3}
+QC_CTRL_ONES = 0xFFFFFFFF
+OPTIONS = {"fusion": 0, "relabel_swap": 1, "use_graph": 2, "tile_bits": 3, "ctas": 4}
+
+GATE_DTYPE = np.dtype([("op", "<i4"), ("qubits", "<i4", (3,)), ("ctrl_state", "<u4"),
+                       ("flags", "<u4"), ("theta", "<f8"), ("m", "<f8", (32,))])
+assert GATE_DTYPE.itemsize == 288
+
+EXPORTS = ["qc_state_create", "qc_state_create_ex", "qc_state_wrap", "qc_state_destroy",
+           "qc_state_init_basis", "qc_state_init_random", "qc_apply_gate", "qc_run_circuit",
+           "qc_state_read", "qc_state_write", "qc_state_canonicalize", "qc_state_sync",
+           "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_last_error", "qc_version"]
+
+
+class QCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"qc status {status}: {msg}")
+        self.status = status
+
+
+class qc_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("device_ptr", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+                ("layout", ctypes.c_int32 * 64), ("layout_is_canonical", ctypes.c_int32),
+                ("last_gates", ctypes.c_int64), ("last_passes", ctypes.c_int64),
+                ("last_launches", ctypes.c_int64), ("last_relabels", ctypes.c_int64),
+                ("last_graph", ctypes.c_int32), ("tile_bits", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libqc.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2303_00123_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, u64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t
+    L.qc_state_create.restype = vp
+    L.qc_state_create.argtypes = [i32, i32]
+    L.qc_state_create_ex.argtypes = [i32, i32, i32, vp, ctypes.POINTER(vp)]
+    L.qc_state_wrap.argtypes = [i32, i32, vp, vp, ctypes.POINTER(vp)]
+    L.qc_state_destroy.argtypes = [vp]
+    L.qc_state_destroy.restype = None
+    L.qc_state_init_basis.argtypes = [vp, u64]
+    L.qc_state_init_random.argtypes = [vp, u64]
+    L.qc_apply_gate.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+    L.qc_run_circuit.argtypes = [vp, vp, sz]
+    L.qc_state_read.argtypes = [vp, u64, u64, vp]
+    L.qc_state_write.argtypes = [vp, u64, u64, vp]
+    L.qc_state_canonicalize.argtypes = [vp]
+    L.qc_state_sync.argtypes = [vp]
+    L.qc_state_norm2.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+    L.qc_set_option.argtypes = [vp, i32, ctypes.c_int64]
+    L.qc_get_info.argtypes = [vp, ctypes.POINTER(qc_info)]
+    L.qc_last_error.restype = ctypes.c_char_p
+    L.qc_version.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        f = getattr(L, name)
+        if name not in ("qc_state_create", "qc_state_destroy", "qc_last_error", "qc_version"):
+            f.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != QC_OK:
+        raise QCError(rc, lib().qc_last_error().decode())
+
+
+def encode_ops(ops: Iterable) -> np.ndarray:
+    """Gate records (objects with name, qubits, theta, matrix, ctrl_state) ->
+    contiguous array of ``qc_gate`` structs."""
+    ops = list(ops)
+    arr = np.zeros(len(ops), dtype=GATE_DTYPE)
+    for i, op in enumerate(ops):
+        name = op.name
+        arr[i]["op"] = OPS[name]
+        q = list(op.qubits) + [0] * (3 - len(op.qubits))
+        arr[i]["qubits"] = q
+        cs = getattr(op, "ctrl_state", None)
+        arr[i]["ctrl_state"] = QC_CTRL_ONES if cs is None else cs
+        th = getattr(op, "theta", None)
+        arr[i]["theta"] = 0.0 if th is None else th
+        m = getattr(op, "matrix", None)
+        if m is not None:
+            m = np.asarray(m, dtype=np.complex128).reshape(-1)
+            flat = np.zeros(32)
+            flat[0:2 * m.size:2] = m.real
+            flat[1:2 * m.size:2] = m.imag
+            arr[i]["m"] = flat
+    return arr
+
+
+class State:
+    """Owning handle of one qc_state (device-resident 2^n amplitudes)."""
+
+    def __init__(self, n: int, precision: str = "c128", device: int = 0,
+                 stream: Optional[int] = None, _handle=None):
+        self.n = n
+        self.precision = precision
+        self.dtype = np.complex128 if precision == "c128" else np.complex64
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = ctypes.c_void_p()
+        _check(lib().qc_state_create_ex(n, PRECISION[precision], device, stream, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def wrap(cls, n: int, precision: str, dev_ptr: int, stream: Optional[int] = None) -> "State":
+        h = ctypes.c_void_p()
+        _check(lib().qc_state_wrap(n, PRECISION[precision], dev_ptr, stream, ctypes.byref(h)))
+        return cls(n, precision, _handle=h)
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().qc_state_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- init
+    def init_random(self, seed: int):
+        _check(lib().qc_state_init_random(self._h, seed))
+
+    def init_basis(self, k: int):
+        _check(lib().qc_state_init_basis(self._h, k))
+
+    # -- the path
+    def apply_gate(self, name: str, qubits: Sequence[int], matrix=None):
+        q = (ctypes.c_int * 3)(*(list(qubits) + [0] * (3 - len(qubits))))
+        mp = None
+        if matrix is not None:
+            m = np.asarray(matrix)
+            if np.iscomplexobj(m):
+                m = np.ascontiguousarray(np.stack([m.real, m.imag], -1).reshape(-1), dtype=np.float64)
+            else:
+                m = np.ascontiguousarray(m, dtype=np.float64).reshape(-1)
+            self._keep = m
+            mp = m.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        _check(lib().qc_apply_gate(self._h, OPS[name], q, mp))
+
+    def run(self, ops) -> None:
+        arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
+        arr = np.ascontiguousarray(arr)
+        _check(lib().qc_run_circuit(self._h, arr.ctypes.data if len(arr) else None, len(arr)))
+
+    # -- I/O
+    def read(self, first: int = 0, count: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if count is None:
+            count = (1 << self.n) - first
+        if out is None:
+            out = np.empty(count, dtype=self.dtype)
+        _check(lib().qc_state_read(self._h, first, count, out.ctypes.data))
+        return out
+
+    def write(self, arr: np.ndarray, first: int = 0):
+        a = np.ascontiguousarray(arr, dtype=self.dtype)
+        _check(lib().qc_state_write(self._h, first, a.size, a.ctypes.data))
+
+    def write_ptr(self, host_ptr: int, count: int, first: int = 0):
+        _check(lib().qc_state_write(self._h, first, count, host_ptr))
+
+    def read_ptr(self, host_ptr: int, count: int, first: int = 0):
+        _check(lib().qc_state_read(self._h, first, count, host_ptr))
+
+    def canonicalize(self):
+        _check(lib().qc_state_canonicalize(self._h))
+
+    def sync(self):
+        _check(lib().qc_state_sync(self._h))
+
+    def norm2(self) -> float:
+        v = ctypes.c_double()
+        _check(lib().qc_state_norm2(self._h, ctypes.byref(v)))
+        return v.value
+
+    def set_option(self, name: str, value: int):
+        _check(lib().qc_set_option(self._h, OPTIONS[name], int(value)))
+
+    def info(self) -> dict:
+        i = qc_info()
+        _check(lib().qc_get_info(self._h, ctypes.byref(i)))
+        return {"n": i.n, "precision": i.precision, "device_ptr": i.device_ptr, "stream": i.stream,
+                "layout": list(i.layout[: i.n]), "layout_is_canonical": bool(i.layout_is_canonical),
+                "last_gates": i.last_gates, "last_passes": i.last_passes,
+                "last_launches": i.last_launches, "last_relabels": i.last_relabels,
+                "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits}
+
+    @property
+    def stream(self) -> int:
+        return self.info()["stream"] or 0
+
+
+def version() -> str:
+    return lib().qc_version().decode()

@@ -1,0 +1,87 @@
+"""CPU-side checks of the C-ABI library: it loads and exports every symbol
+include/qc.h declares; struct layouts agree with the binding; error paths
+work without a GPU.  No compute calls."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2303_00123_b200 as pkg
+from paper_2303_00123_b200 import qc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "qc.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(qc_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    syms = declared_symbols()
+    for s in ("qc_state_create", "qc_apply_gate", "qc_run_circuit", "qc_state_read"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = pkg.lib()
+    missing = [s for s in declared_symbols() if not hasattr(L, s)]
+    assert not missing, missing
+    assert sorted(qc.EXPORTS) == declared_symbols()
+
+
+def test_version_string():
+    assert pkg.version().startswith("qc-b200 1")
+
+
+def test_gate_struct_layout_matches_header():
+    # qc_gate: int32 op, int32 qubits[3], uint32 ctrl_state, uint32 flags,
+    # double theta, double m[32]  -> 288 bytes
+    assert qc.GATE_DTYPE.itemsize == 288
+    assert qc.GATE_DTYPE.fields["theta"][1] == 24
+    assert qc.GATE_DTYPE.fields["m"][1] == 32
+    assert ctypes.sizeof(qc.qc_info) == 4 + 4 + 8 + 8 + 256 + 4 + 4 + 8 * 4 + 4 + 4
+
+
+def test_op_codes_match_header():
+    txt = open(os.path.join(ROOT, "include", "qc.h")).read()
+    for name, code in qc.OPS.items():
+        assert re.search(rf"QC_{name}\s*=\s*{code}\b", txt), name
+
+
+def test_encode_ops_roundtrip():
+    import numpy as np
+    import qcgen
+    ops = [qcgen.Op("CP", (3, 1), theta=0.25), qcgen.Op("U2", (0, 2), matrix=np.eye(4) * 1j),
+           qcgen.Op("CNOT", (1, 2), ctrl_state=0)]
+    a = qc.encode_ops(ops)
+    assert a[0]["op"] == qc.OPS["CP"] and list(a[0]["qubits"][:2]) == [3, 1]
+    assert a[0]["theta"] == 0.25 and a[0]["ctrl_state"] == 1
+    assert a[1]["m"][1] == 1.0 and a[1]["m"][0] == 0.0 and a[1]["m"][2 * 5 + 1] == 1.0
+    assert a[2]["ctrl_state"] == 0
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU error path")
+def test_create_without_gpu_fails_cleanly():
+    L = pkg.lib()
+    assert L.qc_state_create(10, 1) is None
+    assert len(L.qc_last_error()) > 0
+    with pytest.raises(qc.QCError):
+        pkg.State(5, "c128")
+
+
+def test_null_state_is_rejected():
+    L = pkg.lib()
+    assert L.qc_state_sync(None) == qc.QC_ERR_INVALID_ARG
+    assert b"NULL" in L.qc_last_error()
+    L.qc_state_destroy(None)  # no-op

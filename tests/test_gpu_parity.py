@@ -1,0 +1,278 @@
+"""GPU path vs the CPU oracle, through the C ABI (libqc.so).
+
+Tolerances (north star / BASELINE.json): max |amplitude error| <= 1e-12 for
+complex128, <= 1e-5 for complex64; permutation circuits (X/CNOT/SWAP/CCX)
+bit-exact.  Inputs are seeded (qcgen); the oracle never sees device data.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import qcgen
+from qcgen import Op
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-12, "c64": 1e-5}
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def qcmod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2303_00123_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+def gpu_run(pkg, n, prec, ops, seed=qcgen.STATE_SEED, state=None, **opts):
+    with pkg.State(n, prec) as s:
+        for k, v in opts.items():
+            s.set_option(k, v)
+        if state is None:
+            s.init_random(seed)
+        else:
+            s.write(state)
+        s.run(ops)
+        out = s.read()
+        info = s.info()
+    return out, info
+
+
+def ref_run(n, prec, ops, seed=qcgen.STATE_SEED, state=None):
+    st = qcgen.random_state(n, seed=seed, precision=prec) if state is None else state
+    return oracle.run(n, st, ops)
+
+
+def maxerr(a, b):
+    return float(np.abs(a.astype(np.complex128) - b).max()) if a.size else 0.0
+
+
+# -------------------------------------------------------------- generator
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("n", [1, 5, 10, 17])
+def test_device_random_state_is_bit_identical(qcmod, prec, n):
+    with qcmod.State(n, prec) as s:
+        s.init_random(qcgen.STATE_SEED)
+        got = s.read()
+    ref = qcgen.random_state(n, precision=prec)
+    assert got.dtype == ref.dtype and np.array_equal(got.view(np.uint8), ref.view(np.uint8))
+
+
+# ---------------------------------------------------------- per-gate path
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_every_gate_every_position_unfused(qcmod, prec):
+    """qc_apply_gate: each kind on every qubit / ordered pair (all stride classes)."""
+    n = 7
+    rng = np.random.default_rng(1)
+    phi = qcgen.random_state(n, seed=2, precision=prec)
+    V = qcgen.random_unitary(2, rng)
+    W = qcgen.random_unitary(4, rng)
+    cases = []
+    for q in range(n):
+        for name in ("H", "X", "Y", "Z"):
+            cases.append((name, (q,), None))
+        for name in ("P", "RX", "RY", "RZ"):
+            cases.append((name, (q,), float(rng.uniform(-7, 7))))
+        cases.append(("U1", (q,), V))
+    for a in range(n):
+        for b in range(n):
+            if a == b:
+                continue
+            cases += [("CNOT", (a, b), None), ("CZ", (a, b), None),
+                      ("CP", (a, b), float(rng.uniform(-7, 7))), ("CU1", (a, b), V),
+                      ("U2", (a, b), W)]
+            if a < b:
+                cases.append(("SWAP", (a, b), None))
+    for c0, c1, t in ((0, 1, 2), (6, 0, 3), (2, 5, 1), (4, 3, 6)):
+        cases.append(("CCX", (c0, c1, t), None))
+    with qcmod.State(n, prec) as s:
+        s.set_option("relabel_swap", 0)
+        for name, qs, arg in cases:
+            s.write(phi)
+            if arg is None:
+                s.apply_gate(name, qs)
+                op = Op(name, qs)
+            elif isinstance(arg, float):
+                s.apply_gate(name, qs, np.array([arg]))
+                op = Op(name, qs, theta=arg)
+            else:
+                s.apply_gate(name, qs, arg)
+                op = Op(name, qs, matrix=arg)
+            got = s.read()
+            ref = oracle.run(n, phi, [op])
+            if name in ("X", "CNOT", "SWAP", "CCX"):
+                assert np.array_equal(got.astype(np.complex128), ref), (name, qs)
+            else:
+                assert maxerr(got, ref) <= TOL[prec], (name, qs, maxerr(got, ref))
+
+
+@pytest.mark.parametrize("fusion", [0, 1])
+def test_paper_index_tables_on_gpu(qcmod, fusion):
+    """fig:1q / fig:ctrl-1q / fig:dctrl-1q
+    through the device path, n=3 (fusion needs n>=4: n=3 runs unfused)."""
+    with open(os.path.join(GOLD, "fig_index_tables.json")) as f:
+        tab = json.load(f)
+    n = 3
+
+    def basis(k):
+        v = np.zeros(8, complex)
+        v[k] = 1
+        return v
+
+    for c in tab["fig_1q"]["cases"]:
+        for a, b in zip(c["a"], c["b"]):
+            out, _ = gpu_run(qcmod, n, "c128", [Op("X", (c["q"],))], state=basis(a), fusion=fusion)
+            assert np.array_equal(out, basis(b))
+    for c in tab["fig_ctrl_1q"]["cases"]:
+        for a, b in zip(c["a"], c["b"]):
+            out, _ = gpu_run(qcmod, n, "c128", [Op("CNOT", (c["qc"], c["qt"]), ctrl_state=c["ctrl"])],
+                             state=basis(a), fusion=fusion)
+            assert np.array_equal(out, basis(b))
+    c = tab["fig_dctrl_1q"]["cases"][0]
+    for x in range(8):
+        out, _ = gpu_run(qcmod, n, "c128", [Op("CCX", tuple(c["qc"]) + (c["qt"],))],
+                         state=basis(x), fusion=fusion)
+        exp = {6: 7, 7: 6}.get(x, x)
+        assert np.array_equal(out, basis(exp))
+
+
+# ---------------------------------------------------------- random circuits
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("n,tile_bits", [(4, 0), (5, 4), (8, 0), (8, 5), (11, 6), (12, 0),
+                                         (13, 7), (14, 0), (16, 9), (18, 0)])
+def test_random_circuits_fused(qcmod, prec, n, tile_bits):
+    ops = qcgen.random_circuit(n, 200, seed=100 + n)
+    got, info = gpu_run(qcmod, n, prec, ops, tile_bits=tile_bits)
+    ref = ref_run(n, prec, ops)
+    assert maxerr(got, ref) <= TOL[prec], (maxerr(got, ref), info)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("n", [2, 6, 13])
+def test_random_circuits_unfused(qcmod, prec, n):
+    ops = qcgen.random_circuit(n, 200, seed=300 + n)
+    got, _ = gpu_run(qcmod, n, prec, ops, fusion=0)
+    assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec]
+
+
+@pytest.mark.parametrize("fusion", [0, 1])
+@pytest.mark.parametrize("relabel", [0, 1])
+@pytest.mark.parametrize("n,tile_bits", [(6, 0), (12, 0), (15, 8)])
+def test_permutation_circuits_bit_exact(qcmod, fusion, relabel, n, tile_bits):
+    ops = qcgen.random_circuit(n, 300, seed=7 + n, kinds=("X", "CNOT", "SWAP", "CCX"))
+    for prec in ("c128", "c64"):
+        got, _ = gpu_run(qcmod, n, prec, ops, fusion=fusion, relabel_swap=relabel, tile_bits=tile_bits)
+        ref = ref_run(n, prec, ops)
+        assert np.array_equal(got.astype(np.complex128), ref)
+
+
+# ---------------------------------------------------------- paper workloads
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_qft_c1_n10(qcmod, prec):
+    """Config C1: QFT on 10 qubits, random initial state (both signs)."""
+    n = 10
+    for sign in (-1, +1):
+        ops = qcgen.qft(n, sign=sign)
+        got, info = gpu_run(qcmod, n, prec, ops)
+        assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec]
+        assert info["last_passes"] == 1  # whole circuit in one launch (n <= tile)
+
+
+def test_tfxy_c2_n20_s10(qcmod):
+    """Config C2: TFXY 1D Trotter circuit, 20 qubits, 10 steps, complex double."""
+    n = 20
+    ops = qcgen.tfxy(n, 10)
+    got, info = gpu_run(qcmod, n, "c128", ops)
+    assert maxerr(got, ref_run(n, "c128", ops)) <= 1e-12
+    assert info["last_gates"] == 1178
+
+
+@pytest.mark.parametrize("n", [14, 17])
+def test_qft_multi_pass_with_relabel(qcmod, n):
+    ops = qcgen.qft(n)
+    got, info = gpu_run(qcmod, n, "c128", ops)
+    assert info["last_relabels"] == n // 2 and not info["layout_is_canonical"]
+    assert maxerr(got, ref_run(n, "c128", ops)) <= 1e-12
+
+
+def test_tfxy_parity_sector_exact_zero_on_gpu(qcmod):
+    n = 16
+    st = qcgen.random_state_even_parity(n, seed=5)
+    got, _ = gpu_run(qcmod, n, "c128", qcgen.tfxy(n, 3), state=st)
+    w = np.array([bin(i).count("1") & 1 for i in range(1 << n)])
+    assert np.all(got[w == 1] == 0)
+
+
+# ---------------------------------------------------------- state plumbing
+def test_graph_replay_matches(qcmod):
+    n = 15
+    ops = qcgen.random_circuit(n, 120, seed=42)
+    inv = qcgen.inverse(ops)
+    with qcmod.State(n, "c128") as s:
+        s.init_random(1)
+        ref0 = s.read()
+        for _ in range(3):  # 1st run direct, 2nd+ graph replay
+            s.run(ops)
+            s.run(inv)
+        assert s.info()["last_graph"]
+        assert maxerr(s.read(), ref0) <= 1e-12
+
+
+def test_read_write_ranges_and_canonicalize(qcmod):
+    n = 12
+    with qcmod.State(n, "c128") as s:
+        s.init_random(9)
+        s.run(qcgen.qft(n))
+        full = s.read()
+        assert not s.info()["layout_is_canonical"]
+        part = s.read(100, 333)
+        assert np.array_equal(part, full[100:433])
+        x = (np.arange(50) + 1j).astype(np.complex128)
+        s.write(x, first=1000)
+        full[1000:1050] = x
+        assert np.array_equal(s.read(), full)
+        s.canonicalize()
+        assert s.info()["layout_is_canonical"]
+        assert np.array_equal(s.read(), full)
+        ref_n2 = np.vdot(full, full).real
+        assert abs(s.norm2() - ref_n2) <= 1e-14 * ref_n2
+
+
+def test_invalid_ops_leave_state_unchanged(qcmod):
+    from paper_2303_00123_b200 import QCError
+    n = 6
+    with qcmod.State(n, "c128") as s:
+        s.init_random(3)
+        before = s.read()
+        bad = [Op("H", (0,)), Op("CNOT", (1, 2))]
+        arr = qcmod.encode_ops(bad)
+        arr[1]["qubits"][1] = 1  # repeated qubit
+        with pytest.raises(QCError) as e:
+            s.run(arr)
+        assert e.value.status == 1
+        arr = qcmod.encode_ops(bad)
+        arr[1]["qubits"][0] = 6  # out of range
+        with pytest.raises(QCError):
+            s.run(arr)
+        with pytest.raises(QCError):
+            s.run([Op("RX", (0,), theta=float("inf"))])
+        assert np.array_equal(s.read(), before)
+
+
+def test_norm_preserved_and_inverse(qcmod):
+    n = 20
+    ops = qcgen.random_circuit(n, 150, seed=11)
+    with qcmod.State(n, "c128") as s:
+        s.init_random(2)
+        n0 = s.norm2()
+        s.run(ops)
+        assert abs(s.norm2() - n0) < 1e-12
+        s.run(qcgen.inverse(ops))
+        s.canonicalize()
+        ref = qcgen.random_state(n, seed=2)
+        assert maxerr(s.read(), ref) <= 1e-12
