@@ -100,7 +100,13 @@ typedef enum {
     QC_OPT_RELABEL_SWAP = 1,  /* 1 (default): SWAP = relabel (0 bytes moved); 0: data move  */
     QC_OPT_USE_GRAPH = 2,     /* 1 (default): replay repeated circuits as CUDA graphs       */
     QC_OPT_TILE_BITS = 3,     /* 0 (default): auto (64 KiB tiles); else 4..13               */
-    QC_OPT_CTAS = 4           /* 0 (default): one CTA per SM; else grid size of fused passes */
+    QC_OPT_CTAS = 4,          /* 0 (default): one CTA per SM; else grid size of fused passes */
+    QC_OPT_BLOCK_FUSION = 5,  /* 1 (default): merge gates on <= 2 qubits into exact blocks    */
+    QC_OPT_JIT = 6,           /* 1 (default): specialise repeated fused plans with NVRTC;
+                                 0: never (AOT interpreting kernel); 2: from the first run  */
+    QC_OPT_ROW_BITS = 7,      /* 0 (default): auto; else contiguous row bits of a fused tile */
+    QC_OPT_TMA_MODE = 8       /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
+                                 request); 1: one cp.async.bulk per row                      */
 } qc_option;
 
 /* Counters of the most recent qc_run_circuit / qc_apply_gate. */
@@ -117,6 +123,9 @@ typedef struct qc_info {
     int64_t last_relabels;    /* SWAPs applied as relabels                      */
     int32_t last_graph;       /* 1 if the last run replayed a CUDA graph        */
     int32_t tile_bits;        /* k of the last fused run                        */
+    int64_t last_blocks;      /* ops after block fusion (fused runs)            */
+    int32_t last_jit;         /* 1 if the last run used NVRTC-specialised passes */
+    int32_t reserved;
 } qc_info;
 
 /* ---------------------------------------------------------------- lifetime */

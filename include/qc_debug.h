@@ -1,0 +1,40 @@
+/*
+ * qc_debug.h -- host-only introspection of libqc's planner (no GPU needed).
+ *
+ * qc_debug_plan lowers an op list with the canonical layout, applies block
+ * fusion and the fused-pass planner exactly as qc_run_circuit would, and
+ * reports the plan's shape.  With compile_jit != 0 it also generates and
+ * NVRTC-compiles the specialised kernel of every pass for sm_100a (no launch).
+ * Used by the CPU test-suite to check planner invariants and the code
+ * generator; not part of the hot path.
+ */
+#ifndef QC_DEBUG_H_
+#define QC_DEBUG_H_
+#include "qc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qc_plan_stats {
+    int64_t gates;        /* input gates                                    */
+    int64_t relabels;     /* SWAPs turned into relabels                     */
+    int64_t blocks;       /* ops after block fusion                         */
+    int64_t passes;       /* fused tile passes                              */
+    int64_t substages;    /* register sub-stages over all passes            */
+    int64_t fused_ops;    /* encoded ops over all passes                    */
+    int64_t phase_runs;   /* phase-run ops over all passes                  */
+    int64_t blob_bytes;   /* packed op blob bytes                           */
+    int32_t tile_bits;
+    int32_t jit_compiled; /* passes compiled by NVRTC (compile_jit != 0)    */
+} qc_plan_stats;
+
+/* tile_bits 0 = default.  errbuf (may be NULL) receives a message on error. */
+qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
+                        int block_fusion, int compile_jit, qc_plan_stats* out, char* errbuf,
+                        size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

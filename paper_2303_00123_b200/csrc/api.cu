@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "qc_internal.h"
+#include "../../include/qc_debug.h"
 
 using namespace qc;
 
@@ -38,8 +39,13 @@ struct PlanEntry {
   std::vector<qc_gate> ops;          // exact copy (collision check)
   std::vector<int> layout_in, layout_out;
   std::vector<PassDesc> passes;
-  void* d_subs = nullptr;
-  void* d_ops = nullptr;
+  void* d_blob = nullptr;
+  int64_t fused_gates = 0;
+  std::shared_ptr<FusedPlan> ir;     // kept for JIT specialisation
+  std::vector<JitKernel> jit;
+  int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
+  QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
+  bool dbl = true;
   int64_t relabels = 0;
   int uses = 0;
   cudaGraph_t graph = nullptr;
@@ -49,8 +55,7 @@ struct PlanEntry {
   ~PlanEntry() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    if (d_subs) cudaFree(d_subs);
-    if (d_ops) cudaFree(d_ops);
+    if (d_blob) cudaFree(d_blob);
   }
 };
 
@@ -69,10 +74,14 @@ struct qc_state {
   int layout[64];
   bool failed = false;
   // options
-  int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0;
+  int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0, block_fusion = 1, jit = 1;
+  int row_bits = 0, tma_mode = 0;
+  std::string jit_error;
   // stats
   int64_t last_gates = 0, last_passes = 0, last_launches = 0, last_relabels = 0;
   int last_graph = 0, last_k = 0;
+  int64_t last_blocks = 0;
+  int last_jit = 0;
   // plan cache
   std::unordered_map<uint64_t, std::unique_ptr<PlanEntry>> plans;
   cudaStream_t cap_stream = nullptr;
@@ -195,22 +204,17 @@ uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint6
   return h;
 }
 
-template <typename T>
-void to_prec(const FOpT<double>& a, FOpT<T>& b) {
-  std::memcpy(&b, &a, offsetof(FOpT<double>, m));
-  for (int i = 0; i < 32; ++i) b.m[i] = (T)a.m[i];
-}
-
 // Build (or fetch) the fused plan for this op list and the current layout.
 qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
   const int n = s->n;
   int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
   if (k > n) k = n;
-  int rb = s->dbl ? 5 : 6;
+  int rb = s->row_bits ? s->row_bits : (s->dbl ? 5 : 6);
   if (rb > k - 2) rb = k - 2;
   if (rb < 1) rb = 1;
   const int ctas = s->ctas ? s->ctas : sm_count();
   const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
+                        ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)(s->jit == 2) << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^
                         ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
   const uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
   auto it = s->plans.find(key);
@@ -244,28 +248,25 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   }
   e->layout_out.assign(lay, lay + n);
   if (!gates.empty()) {
-    FusedPlan fp = plan_fused(n, k, rb, gates);
-    if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
-    for (auto& p : fp.passes) e->passes.push_back(p.desc);
-    const size_t sb = fp.subs.size() * sizeof(SubStageDesc);
-    cudaError_t ce = cudaMalloc(&e->d_subs, sb);
-    if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
-    ce = cudaMemcpy(e->d_subs, fp.subs.data(), sb, cudaMemcpyHostToDevice);
-    if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
-    if (s->dbl) {
-      const size_t ob = fp.ops.size() * sizeof(FOpT<double>);
-      ce = cudaMalloc(&e->d_ops, ob);
+    std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates) : gates;
+    e->fused_gates = (int64_t)blocks.size();
+    if (!blocks.empty()) {
+      FusedPlan fp = plan_fused(n, k, rb, blocks);
+      if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
+      const bool g4 = s->tma_mode == 0 && make_row_tmap(s->d, n, rb, s->dbl, &e->tmap);
+      for (auto& p : fp.passes) {
+        p.desc.g4 = g4 ? 1 : 0;
+        p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
+      }
+      std::vector<uint8_t> blob = pack_plan(fp, s->dbl);
+      for (auto& p : fp.passes) e->passes.push_back(p.desc);
+      e->dbl = s->dbl;
+      e->ir = std::make_shared<FusedPlan>(std::move(fp));
+      cudaError_t ce = cudaMalloc(&e->d_blob, blob.size());
       if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
-      ce = cudaMemcpy(e->d_ops, fp.ops.data(), ob, cudaMemcpyHostToDevice);
-    } else {
-      std::vector<FOpT<float>> f(fp.ops.size());
-      for (size_t i = 0; i < f.size(); ++i) to_prec(fp.ops[i], f[i]);
-      const size_t ob = f.size() * sizeof(FOpT<float>);
-      ce = cudaMalloc(&e->d_ops, ob);
-      if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
-      ce = cudaMemcpy(e->d_ops, f.data(), ob, cudaMemcpyHostToDevice);
+      ce = cudaMemcpy(e->d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+      if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
     }
-    if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
   }
   PlanEntry* raw = e.get();
   if (s->plans.size() > 64) s->plans.clear();
@@ -275,8 +276,10 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
 }
 
 int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) {
-  for (const PassDesc& pd : e->passes) {
-    const int r = launch_fused_pass(s->d, s->dbl, pd, e->d_subs, e->d_ops, e->ctas, st);
+  for (size_t i = 0; i < e->passes.size(); ++i) {
+    const PassDesc& pd = e->passes[i];
+    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], s->d, pd, e->tmap, e->ctas, st)
+                                      : launch_fused_pass(s->d, s->dbl, pd, e->d_blob, e->tmap, e->ctas, st);
     if (r) return r;
   }
   return 0;
@@ -285,7 +288,7 @@ int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) {
 qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   static bool configured[2] = {false, false};
   if (!configured[s->dbl]) {
-    const int r = fused_configure(s->dbl, 0);
+    const int r = fused_configure(s->dbl);
     if (r) return cuda_fail(s, r, "cudaFuncSetAttribute(fused)");
     configured[s->dbl] = true;
   }
@@ -294,6 +297,16 @@ qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   if (st != QC_OK) return st;
   e->uses++;
   s->last_graph = 0;
+  if (e->jit_state == 0 && e->ir && (s->jit == 2 || (s->jit == 1 && e->uses >= 2))) {
+    std::string err;
+    if (jit_build(*e->ir, s->dbl, e->jit, err)) {
+      e->jit_state = 1;
+    } else {
+      e->jit_state = -1;
+      s->jit_error = err;
+      if (s->jit == 2) return fail(QC_ERR_UNSUPPORTED, "JIT specialisation failed: %s", err.c_str());
+    }
+  }
   int r = 0;
   if (s->use_graph && e->uses >= 2 && !e->passes.empty()) {
     if (!e->exec) {
@@ -322,6 +335,8 @@ qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   s->last_launches = (int64_t)e->passes.size();
   s->last_relabels = e->relabels;
   s->last_k = e->tile_bits;
+  s->last_blocks = e->fused_gates;
+  s->last_jit = e->jit_state == 1 ? 1 : 0;
   return QC_OK;
 }
 
@@ -342,6 +357,7 @@ qc_status run_unfused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   s->last_launches = launches;
   s->last_relabels = relabels;
   s->last_graph = 0;
+  s->last_jit = 0;
   s->last_k = 0;
   return QC_OK;
 }
@@ -628,6 +644,19 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       if (v < 0 || v > 65535) return fail(QC_ERR_INVALID_ARG, "ctas out of range");
       s->ctas = (int)v;
       break;
+    case QC_OPT_BLOCK_FUSION: s->block_fusion = v != 0; break;
+    case QC_OPT_ROW_BITS:
+      if (v != 0 && (v < 1 || v > 11)) return fail(QC_ERR_INVALID_ARG, "row bits must be 0 or 1..11");
+      s->row_bits = (int)v;
+      break;
+    case QC_OPT_TMA_MODE:
+      if (v < 0 || v > 1) return fail(QC_ERR_INVALID_ARG, "tma mode must be 0 or 1");
+      s->tma_mode = (int)v;
+      break;
+    case QC_OPT_JIT:
+      if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "jit must be 0, 1 or 2");
+      s->jit = (int)v;
+      break;
     default: return fail(QC_ERR_INVALID_ARG, "unknown option %d", (int)opt);
   }
   return QC_OK;
@@ -648,7 +677,64 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
   out->last_relabels = s->last_relabels;
   out->last_graph = s->last_graph;
   out->tile_bits = s->last_k;
+  out->last_blocks = s->last_blocks;
+  out->last_jit = s->last_jit;
   return QC_OK;
 }
 
 }  // extern "C"
+
+extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
+                                   int block_fusion, int compile_jit, qc_plan_stats* out, char* errbuf,
+                                   size_t errlen) {
+  auto err = [&](qc_status st, const std::string& m) {
+    fail(st, "%s", m.c_str());
+    if (errbuf && errlen) snprintf(errbuf, errlen, "%s", m.c_str());
+    return st;
+  };
+  if (!out) return err(QC_ERR_INVALID_ARG, "out is NULL");
+  std::memset(out, 0, sizeof *out);
+  if (n < 1 || n > kMaxQubits) return err(QC_ERR_INVALID_ARG, "bad n");
+  if (n_ops && !ops) return err(QC_ERR_INVALID_ARG, "ops is NULL");
+  for (size_t i = 0; i < n_ops; ++i)
+    if (validate_gate(n, ops[i], i) != QC_OK) return err(QC_ERR_INVALID_ARG, g_err);
+  const bool dbl = p == QC_COMPLEX128;
+  int k = tile_bits ? tile_bits : (dbl ? 12 : 13);
+  if (k > n) k = n;
+  int rb = dbl ? 5 : 6;
+  if (rb > k - 2) rb = k - 2;
+  if (rb < 1) rb = 1;
+  int lay[64];
+  for (int q = 0; q < n; ++q) lay[q] = n - 1 - q;
+  std::vector<PGate> gates;
+  for (size_t i = 0; i < n_ops; ++i) {
+    if (ops[i].op == QC_SWAP) {
+      std::swap(lay[ops[i].qubits[0]], lay[ops[i].qubits[1]]);
+      out->relabels++;
+      continue;
+    }
+    gates.push_back(lower(ops[i], lay));
+  }
+  out->gates = (int64_t)n_ops;
+  out->tile_bits = k;
+  std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates) : gates;
+  out->blocks = (int64_t)blocks.size();
+  if (blocks.empty()) return QC_OK;
+  FusedPlan fp = plan_fused(n, k, rb, blocks);
+  if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
+  out->passes = (int64_t)fp.passes.size();
+  for (auto& pp : fp.passes) {
+    out->substages += (int64_t)pp.subs.size();
+    out->fused_ops += (int64_t)pp.ops.size();
+    for (auto& o : pp.ops) out->phase_runs += o.h.kind == F_PRUN;
+  }
+  std::vector<uint8_t> blob = pack_plan(fp, dbl);
+  out->blob_bytes = (int64_t)blob.size();
+  if (compile_jit) {
+    std::string e;
+    int compiled = 0;
+    if (!jit_compile_only(fp, dbl, compiled, e)) return err(QC_ERR_UNSUPPORTED, e);
+    out->jit_compiled = compiled;
+  }
+  return QC_OK;
+}

@@ -27,7 +27,9 @@ OPS = {"H": 0, "X": 1, "Y": 2, "Z": 3, "P": 4, "RX": 5, "RY": 6, "RZ": 7, "CNOT"
 ARITY = {"H": 1, "X": 1, "Y": 1, "Z": 1, "P": 1, "RX": 1, "RY": 1, "RZ": 1, "CNOT": 2,
          "CZ": 2, "CP": 2, "SWAP": 2, "U1": 1, "CU1": 2, "U2": 2, "CCX": 3}
 QC_CTRL_ONES = 0xFFFFFFFF
-OPTIONS = {"fusion": 0, "relabel_swap": 1, "use_graph": 2, "tile_bits": 3, "ctas": 4}
+OPTIONS = {"fusion": 0, "relabel_swap": 1, "use_graph": 2, "tile_bits": 3, "ctas": 4,
+           "block_fusion": 5, "jit": 6, "row_bits": 7,
+           "tma_mode": 8}
 
 GATE_DTYPE = np.dtype([("op", "<i4"), ("qubits", "<i4", (3,)), ("ctrl_state", "<u4"),
                        ("flags", "<u4"), ("theta", "<f8"), ("m", "<f8", (32,))])
@@ -51,8 +53,20 @@ class qc_info(ctypes.Structure):
                 ("layout", ctypes.c_int32 * 64), ("layout_is_canonical", ctypes.c_int32),
                 ("last_gates", ctypes.c_int64), ("last_passes", ctypes.c_int64),
                 ("last_launches", ctypes.c_int64), ("last_relabels", ctypes.c_int64),
-                ("last_graph", ctypes.c_int32), ("tile_bits", ctypes.c_int32)]
+                ("last_graph", ctypes.c_int32), ("tile_bits", ctypes.c_int32),
+                ("last_blocks", ctypes.c_int64), ("last_jit", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
+
+class qc_plan_stats(ctypes.Structure):
+    _fields_ = [("gates", ctypes.c_int64), ("relabels", ctypes.c_int64), ("blocks", ctypes.c_int64),
+                ("passes", ctypes.c_int64), ("substages", ctypes.c_int64),
+                ("fused_ops", ctypes.c_int64), ("phase_runs", ctypes.c_int64),
+                ("blob_bytes", ctypes.c_int64), ("tile_bits", ctypes.c_int32),
+                ("jit_compiled", ctypes.c_int32)]
+
+
+DEBUG_EXPORTS = ["qc_debug_plan"]
 
 _lib = None
 
@@ -83,6 +97,9 @@ def lib() -> ctypes.CDLL:
     L.qc_state_norm2.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     L.qc_set_option.argtypes = [vp, i32, ctypes.c_int64]
     L.qc_get_info.argtypes = [vp, ctypes.POINTER(qc_info)]
+    L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
+                                ctypes.c_char_p, sz]
+    L.qc_debug_plan.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
     L.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -227,11 +244,27 @@ class State:
                 "layout": list(i.layout[: i.n]), "layout_is_canonical": bool(i.layout_is_canonical),
                 "last_gates": i.last_gates, "last_passes": i.last_passes,
                 "last_launches": i.last_launches, "last_relabels": i.last_relabels,
-                "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits}
+                "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits,
+                "last_blocks": i.last_blocks, "last_jit": bool(i.last_jit)}
 
     @property
     def stream(self) -> int:
         return self.info()["stream"] or 0
+
+
+def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_fusion: bool = True,
+               compile_jit: bool = False) -> dict:
+    """Plan an op list on the host (no GPU) and report its shape; optionally
+    NVRTC-compile every pass's specialised kernel (qc_debug.h)."""
+    arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
+    arr = np.ascontiguousarray(arr)
+    st = qc_plan_stats()
+    eb = ctypes.create_string_buffer(4096)
+    rc = lib().qc_debug_plan(n, PRECISION[precision], arr.ctypes.data if len(arr) else None, len(arr),
+                             tile_bits, int(block_fusion), int(compile_jit), ctypes.byref(st), eb, 4096)
+    if rc != QC_OK:
+        raise QCError(rc, eb.value.decode())
+    return {f: getattr(st, f) for f, _ in qc_plan_stats._fields_}
 
 
 def version() -> str:

@@ -276,3 +276,47 @@ def test_norm_preserved_and_inverse(qcmod):
         s.canonicalize()
         ref = qcgen.random_state(n, seed=2)
         assert maxerr(s.read(), ref) <= 1e-12
+
+
+# ---------------------------------------------------------- NVRTC-specialised passes
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("n,tile_bits", [(5, 4), (10, 0), (14, 7), (17, 9), (19, 0)])
+def test_random_circuits_jit(qcmod, prec, n, tile_bits):
+    ops = qcgen.random_circuit(n, 200, seed=500 + n)
+    got, info = gpu_run(qcmod, n, prec, ops, tile_bits=tile_bits, jit=2)
+    assert info["last_jit"], info
+    assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec]
+
+
+def test_permutation_circuit_jit_bit_exact(qcmod):
+    n = 15
+    ops = qcgen.random_circuit(n, 300, seed=77, kinds=("X", "CNOT", "SWAP", "CCX"))
+    for prec in ("c128", "c64"):
+        got, info = gpu_run(qcmod, n, prec, ops, tile_bits=8, jit=2, relabel_swap=0)
+        assert info["last_jit"]
+        assert np.array_equal(got.astype(np.complex128), ref_run(n, prec, ops))
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_paper_workloads_jit(qcmod, prec):
+    for n, ops in ((10, qcgen.qft(10)), (16, qcgen.qft(16)), (20, qcgen.tfxy(20, 10))):
+        got, info = gpu_run(qcmod, n, prec, ops, jit=2)
+        assert info["last_jit"]
+        assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec], (n, prec)
+
+
+def test_jit_default_policy_second_run(qcmod):
+    """Default policy: 1st run interprets, 2nd run specialises (then graphs)."""
+    n = 16
+    ops = qcgen.tfxy(n, 3)
+    inv = qcgen.inverse(ops)
+    with qcmod.State(n, "c128") as s:
+        s.init_random(4)
+        s.run(ops)
+        assert not s.info()["last_jit"]
+        s.run(inv)
+        s.run(ops)
+        assert s.info()["last_jit"]
+        s.run(inv)
+        got = s.read()
+    assert maxerr(got, qcgen.random_state(n, seed=4)) <= 1e-12

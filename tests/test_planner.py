@@ -1,0 +1,64 @@
+"""Host-side planner / code-generator checks through qc_debug_plan (no GPU)."""
+import numpy as np
+import pytest
+
+import qcgen
+from paper_2303_00123_b200 import qc
+
+
+def test_debug_symbol_exported():
+    for s in qc.DEBUG_EXPORTS:
+        assert hasattr(qc.lib(), s)
+
+
+def test_qft30_plan_shape():
+    st = qc.debug_plan(30, qcgen.qft(30))
+    assert st["gates"] == 480 and st["relabels"] == 15
+    # 7 high tile bits per pass: H(0..6), H(7..13), H(14..20), H(21..29)
+    assert st["passes"] == 4
+    assert st["phase_runs"] > 0
+    assert st["blob_bytes"] > 0
+
+
+def test_tfxy_block_fusion_merges_pair_blocks():
+    st = qc.debug_plan(20, qcgen.tfxy(20, 10))
+    raw = qc.debug_plan(20, qcgen.tfxy(20, 10), block_fusion=False)
+    assert st["gates"] == 1178
+    # every pair block (CNOT RX RZ CNOT + adjacent RZ layers) becomes one op
+    assert st["blocks"] < raw["blocks"] / 4
+    assert st["passes"] <= raw["passes"] + 2
+
+
+def test_permutation_pairs_cancel_exactly():
+    ops = [qcgen.Op("CNOT", (1, 3)), qcgen.Op("CNOT", (1, 3)), qcgen.Op("X", (2,)), qcgen.Op("X", (2,))]
+    st = qc.debug_plan(6, ops)
+    assert st["blocks"] == 0 and st["passes"] == 0
+
+
+@pytest.mark.parametrize("n,tile", [(4, 0), (9, 5), (16, 8), (20, 0)])
+def test_every_gate_is_planned(n, tile):
+    ops = qcgen.random_circuit(n, 150, seed=n)
+    st = qc.debug_plan(n, ops, tile_bits=tile, block_fusion=False)
+    nonswap = sum(1 for o in ops if o.name != "SWAP")
+    assert st["blocks"] == nonswap
+    # every non-SWAP gate is encoded exactly once (phase runs absorb several)
+    assert st["fused_ops"] <= nonswap and st["fused_ops"] > 0
+
+
+def test_invalid_ops_rejected():
+    with pytest.raises(qc.QCError):
+        qc.debug_plan(3, [qcgen.Op("H", (0,))] + [qcgen.Op("CNOT", (1, 2))], tile_bits=2)
+    arr = qc.encode_ops([qcgen.Op("CNOT", (1, 2))])
+    arr[0]["qubits"][1] = 1
+    with pytest.raises(qc.QCError):
+        qc.debug_plan(4, arr)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_jit_codegen_compiles_for_sm100a(prec):
+    """Generated specialised kernels compile with NVRTC for sm_100a (all op
+    kinds / patterns / predicate sources appear in this mix)."""
+    n = 14
+    ops = qcgen.random_circuit(n, 120, seed=5) + qcgen.qft(n) + qcgen.tfxy(n, 2)
+    st = qc.debug_plan(n, ops, precision=prec, tile_bits=10, compile_jit=True)
+    assert st["jit_compiled"] == st["passes"] > 1
