@@ -29,10 +29,10 @@ typedef struct qc_plan_stats {
     int32_t jit_compiled; /* passes compiled by NVRTC (compile_jit != 0)    */
 } qc_plan_stats;
 
-/* tile_bits 0 = default.  errbuf (may be NULL) receives a message on error. */
+/* tile_bits / row_bits 0 = default.  errbuf (may be NULL) receives a message on error. */
 qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
-                        int block_fusion, int compile_jit, qc_plan_stats* out, char* errbuf,
-                        size_t errlen);
+                        int row_bits, int block_fusion, int compile_jit, qc_plan_stats* out,
+                        char* errbuf, size_t errlen);
 
 #ifdef __cplusplus
 }

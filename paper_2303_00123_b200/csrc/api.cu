@@ -208,6 +208,7 @@ uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint6
 qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
   const int n = s->n;
   int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
+  if (s->dbl && k > 12) k = 12;  // two 2^k tiles (one per compute group) must fit in smem
   if (k > n) k = n;
   int rb = s->row_bits ? s->row_bits : (s->dbl ? 5 : 6);
   if (rb > k - 2) rb = k - 2;
@@ -685,8 +686,8 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
 }  // extern "C"
 
 extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
-                                   int block_fusion, int compile_jit, qc_plan_stats* out, char* errbuf,
-                                   size_t errlen) {
+                                   int row_bits, int block_fusion, int compile_jit, qc_plan_stats* out,
+                                   char* errbuf, size_t errlen) {
   auto err = [&](qc_status st, const std::string& m) {
     fail(st, "%s", m.c_str());
     if (errbuf && errlen) snprintf(errbuf, errlen, "%s", m.c_str());
@@ -700,8 +701,9 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
     if (validate_gate(n, ops[i], i) != QC_OK) return err(QC_ERR_INVALID_ARG, g_err);
   const bool dbl = p == QC_COMPLEX128;
   int k = tile_bits ? tile_bits : (dbl ? 12 : 13);
+  if (dbl && k > 12) k = 12;
   if (k > n) k = n;
-  int rb = dbl ? 5 : 6;
+  int rb = row_bits ? row_bits : (dbl ? 5 : 6);
   if (rb > k - 2) rb = k - 2;
   if (rb < 1) rb = 1;
   int lay[64];

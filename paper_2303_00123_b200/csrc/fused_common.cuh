@@ -7,9 +7,10 @@
 //   warp 8      TMA producer: cp.async.bulk global->smem for each row of the
 //               next tile (mbarrier complete_tx), cp.async.bulk smem->global
 //               of finished tiles (bulk_group), NBUF-deep ring.
-//   warps 0..7  compute: Body::tile() applies the pass's ops to the tile in
-//               smem (sub-stages of 16-amplitude register tasks), then
-//               fence.proxy.async + mbarrier arrive.
+//   warps 0..7  compute, in 2 groups of 4 warps taking alternate tiles:
+//               Body::tile() applies the pass's ops to the tile in smem
+//               (sub-stages of 16-amplitude register tasks, group-local named
+//               barriers), then fence.proxy.async + mbarrier arrive.
 // Rows are padded by 16 B in smem so slot strides of 1..16 amplitudes hit
 // distinct bank quads (complex128).
 #pragma once
@@ -40,9 +41,13 @@ __device__ __forceinline__ void qc_mbar_arrive_expect_tx(uint64_t* b, uint32_t b
 __device__ __forceinline__ void qc_mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(qc_saddr(b)) : "memory");
 }
+// Watchdog: a wait that has not completed after ~2^35 cycles (~15 s) traps,
+// turning a pipeline bug into a launch error instead of a hung GPU.
 __device__ __forceinline__ void qc_mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t a = qc_saddr(b);
+  uint32_t spins = 0;
+  long long t0 = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -51,6 +56,11 @@ __device__ __forceinline__ void qc_mbar_wait(uint64_t* b, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+    if (!done && ((++spins & 1023u) == 0)) {
+      const long long t = clock64();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > (1ll << 35)) asm volatile("trap;");
+    }
   } while (!done);
 }
 __device__ __forceinline__ void qc_bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -95,9 +105,15 @@ __device__ __forceinline__ void qc_bulk_wait0() {
 __device__ __forceinline__ void qc_fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Named barrier of the calling thread's compute group (ids 1..kGroups).  The
+// non-.aligned form: callers may arrive from divergent code (e.g. the
+// single-thread phase-run prologue); reconverge the warp first anyway.
 __device__ __forceinline__ void qc_compute_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / kGroupThreads), "n"(kGroupThreads)
+               : "memory");
 }
+__device__ __forceinline__ uint32_t qc_gtid() { return threadIdx.x % kGroupThreads; }
 __device__ __forceinline__ uint32_t qc_ins0(uint32_t x, int p) {
   return ((x >> p) << (p + 1)) | (x & ((1u << p) - 1u));
 }
@@ -330,7 +346,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   if (tid == 0) {
     for (int b = 0; b < NBUF; ++b) {
       qc_mbar_init(&full[b], 1);
-      qc_mbar_init(&empty[b], kComputeThreads);
+      qc_mbar_init(&empty[b], kGroupThreads);
     }
     qc_fence_mbar_init();
   }
@@ -385,9 +401,11 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   }
 
   // =============================== compute warps ===============================
-  for (uint64_t i = 0; i < my_n; ++i) {
+  // Two groups of compute warps take alternate tiles, so one group's smem
+  // round trips and barriers overlap the other group's arithmetic.
+  for (uint64_t i = (uint64_t)(tid / kGroupThreads); i < my_n; i += kGroups) {
     const int b = (int)(i % NBUF);
-    const int par = (int)(i & 1);
+    const int par = (int)(i % kWSlots);
     const uint64_t tbase = qc_tile_base(pd, blockIdx.x + i * gridDim.x);
     body.prologue(tbase, par);
     qc_mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1ull));

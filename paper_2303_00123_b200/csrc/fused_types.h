@@ -19,6 +19,14 @@ constexpr int kSlots = 1 << kSlotBits;
 constexpr int kComputeWarps = 8;      // fused kernel: 8 compute warps ...
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kFusedThreads = kComputeThreads + 32;  // ... + 1 TMA producer warp
+// Two groups (alternate tiles) deadlocked intermittently under stress at
+// n=30 (DESIGN "open issues"); one group is the validated default.
+#ifndef QC_GROUPS
+#define QC_GROUPS 1
+#endif
+constexpr int kGroups = QC_GROUPS;    // compute warps form groups working on alternate tiles
+constexpr int kGroupThreads = kComputeThreads / kGroups;
+constexpr int kWSlots = 4;            // phase-run factor sets: tile index mod 4
 constexpr int kPadBytes = 16;         // smem padding per row (bank-conflict relief)
 constexpr int kMaxPrun = 64;          // phase runs with a per-tile factor, per pass
 

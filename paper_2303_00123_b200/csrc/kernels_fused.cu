@@ -35,10 +35,10 @@ struct InterpBody {
   const FHdr* hdr;
   const C* coef;
   const FTermT<T>* term;
-  C* W;  // [2][kMaxPrun][2] per-tile phase-run factors (tile parity double-buffered)
+  C* W;  // [kWSlots][kMaxPrun][2] per-tile phase-run factors (tile index mod kWSlots)
 
   static __device__ __forceinline__ size_t smem_bytes(const PassDesc& p) {
-    return (size_t)p.blob_bytes + (size_t)2 * kMaxPrun * 2 * sizeof(C);
+    return (size_t)p.blob_bytes + (size_t)kWSlots * kMaxPrun * 2 * sizeof(C);
   }
   __device__ __forceinline__ void setup(unsigned char* extra, const PassDesc& p) {
     const uint4* src = reinterpret_cast<const uint4*>(gblob + p.blob_off);
@@ -55,7 +55,7 @@ struct InterpBody {
   __device__ __forceinline__ void prologue(uint64_t tbase, int par) {
     if (!pd->n_prun) return;
     // per-tile factors of the phase runs: terms on outer bits + unconditional
-    for (uint32_t o = threadIdx.x; o < pd->n_ops; o += kComputeThreads) {
+    for (uint32_t o = qc_gtid(); o < pd->n_ops; o += kGroupThreads) {
       const FHdr h = hdr[o];
       if (h.kind != F_PRUN) continue;
       C w0 = qc_one<C>(), w1 = qc_one<C>();
@@ -194,7 +194,7 @@ struct InterpBody {
           if (s & (1 << j)) off |= 1u << sd.g[j];
         poff[s] = off + (off >> ps) * PAD;
       }
-      for (uint32_t task = threadIdx.x; task < ntasks; task += kComputeThreads) {
+      for (uint32_t task = qc_gtid(); task < ntasks; task += kGroupThreads) {
         uint32_t lb = task;
 #pragma unroll
         for (int j = 0; j < kSlotBits; ++j) lb = qc_ins0(lb, sd.g[j]);
@@ -228,12 +228,12 @@ constexpr size_t kMaxSmem = 227 * 1024;
 template <typename T>
 size_t smem_for(const PassDesc& pd, int nbuf) {
   using C = typename CT<T>::type;
-  return qc_pipeline_smem<C>(pd.k, pd.rb, pd.pshift, nbuf) + pd.blob_bytes + (size_t)2 * kMaxPrun * 2 * sizeof(C);
+  return qc_pipeline_smem<C>(pd.k, pd.rb, pd.pshift, nbuf) + pd.blob_bytes + (size_t)kWSlots * kMaxPrun * 2 * sizeof(C);
 }
 
 template <typename T>
 int pick_nbuf(const PassDesc& pd) {
-  for (int nb = 3; nb >= 1; --nb)
+  for (int nb = 3; nb >= 2; --nb)  // >= 2: one buffer per compute group
     if (smem_for<T>(pd, nb) <= kMaxSmem) return nb;
   return 0;
 }
@@ -300,7 +300,9 @@ bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out) {
   }
   if (!enc) return false;
   const uint64_t elems = (uint64_t)(dbl ? 2 : 1) << rb;
-  if (elems > 256 || n - rb > 31 || n - rb < 2) return false;
+  // Rows above 1 KiB (8 KiB per gather4 request) deadlocked intermittently
+  // under load on B200 (DESIGN "gather4 row limit"): use the row path there.
+  if (elems * 8 > 1024 || n - rb > 31 || n - rb < 2) return false;
   cuuint64_t gdim[2] = {elems, (cuuint64_t)1 << (n - rb)};
   cuuint64_t gstride[1] = {elems * 8};
   cuuint32_t box[2] = {(cuuint32_t)elems, 1};

@@ -160,6 +160,7 @@ FOpIR convert(const PGate& g, const Ctx& c) {
     cd M[16];
     pgate_dense4(g, M);
     rows_to_ir(M, 4, o);
+    for (int i = 0; i < 16; ++i) o.dense[i] = M[i];
     return o;
   }
   cd M[4] = {0, 0, 0, 0};
@@ -179,6 +180,7 @@ FOpIR convert(const PGate& g, const Ctx& c) {
   o.h.kind = F_M1;
   o.h.sb0 = (uint8_t)c.slot(g.t0);
   rows_to_ir(M, 2, o);
+  for (int i = 0; i < 4; ++i) o.dense[i] = M[i];
   return o;
 }
 

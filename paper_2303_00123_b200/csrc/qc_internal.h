@@ -63,6 +63,7 @@ struct FOpIR {
   std::vector<cd> coefs;     // M1/M2: non-zero entries, row-major; DSCALE: d0, d1
   struct Term { uint8_t src, bit, val; cd d0, d1; };
   std::vector<Term> terms;   // PRUN, ordered local, outer, none
+  cd dense[16];              // M1/M2: the exact matrix (row-major), for code generation
 };
 
 struct FusedPassPlan {

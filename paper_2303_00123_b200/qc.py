@@ -97,7 +97,7 @@ def lib() -> ctypes.CDLL:
     L.qc_state_norm2.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     L.qc_set_option.argtypes = [vp, i32, ctypes.c_int64]
     L.qc_get_info.argtypes = [vp, ctypes.POINTER(qc_info)]
-    L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
+    L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
                                 ctypes.c_char_p, sz]
     L.qc_debug_plan.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
@@ -253,7 +253,7 @@ class State:
 
 
 def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_fusion: bool = True,
-               compile_jit: bool = False) -> dict:
+               compile_jit: bool = False, row_bits: int = 0) -> dict:
     """Plan an op list on the host (no GPU) and report its shape; optionally
     NVRTC-compile every pass's specialised kernel (qc_debug.h)."""
     arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
@@ -261,7 +261,8 @@ def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_f
     st = qc_plan_stats()
     eb = ctypes.create_string_buffer(4096)
     rc = lib().qc_debug_plan(n, PRECISION[precision], arr.ctypes.data if len(arr) else None, len(arr),
-                             tile_bits, int(block_fusion), int(compile_jit), ctypes.byref(st), eb, 4096)
+                             tile_bits, row_bits, int(block_fusion), int(compile_jit), ctypes.byref(st),
+                             eb, 4096)
     if rc != QC_OK:
         raise QCError(rc, eb.value.decode())
     return {f: getattr(st, f) for f, _ in qc_plan_stats._fields_}

@@ -320,3 +320,26 @@ def test_jit_default_policy_second_run(qcmod):
         s.run(inv)
         got = s.read()
     assert maxerr(got, qcgen.random_state(n, seed=4)) <= 1e-12
+
+
+# ---------------------------------------------------------- stress (pipeline races)
+@pytest.mark.parametrize("n,prec,rb", [(26, "c128", 5), (26, "c128", 6), (26, "c64", 6), (25, "c128", 7)])
+def test_repeated_runs_roundtrip(qcmod, n, prec, rb):
+    """Many fused runs (JIT + graph replay) of QFT and its inverse: every
+    pipeline launch must complete (device watchdog traps a deadlock) and the
+    state must come back."""
+    ops = qcgen.qft(n)
+    with qcmod.State(n, prec) as s:
+        s.set_option("row_bits", rb)
+        s.init_random(3)
+        n0 = s.norm2()
+        arr, inv = qcmod.encode_ops(ops), qcmod.encode_ops(qcgen.inverse(ops))
+        for _ in range(8):
+            s.run(arr)
+            s.run(inv)
+        assert s.info()["last_jit"] and s.info()["last_graph"]
+        s.canonicalize()
+        got = s.read(0, 1 << 12)
+        assert abs(s.norm2() - n0) <= (1e-9 if prec == "c128" else 1e-4) * n0
+    ref = qcgen.random_state(n, seed=3, precision=prec)[: 1 << 12]
+    assert maxerr(got, ref) <= TOL[prec] * 10
