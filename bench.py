@@ -221,14 +221,18 @@ def run_ours(args, rank, world, local_rank):
                    "initial_state": "splitmix64 seed 12345 (DESIGN input recipe)",
                    "l2": "flushed (512 MiB write) between timed iterations",
                    "parallelism": f"replicas x{world}", "fused_passes_per_step": passes,
-                   "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"]},
+                   "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"],
+                   "jit_specialised": info["last_jit"], "ops_after_block_fusion": info["last_blocks"]},
         "gpu_launches": int(launches_per_step * args.steps),
-        "roofline": {"bound": "hbm", "kernel": "fused_pass_kernel", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "qc_pass (NVRTC-specialised fused tile pass)",
+                     "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "traffic": None,
                      "bytes_per_launch": 2 * state_bytes,
-                     "avg_launch_ms": avg_launch_ms},
+                     "avg_launch_ms": avg_launch_ms,
+                     "note": "avg launch = timed step time / fused launches per step (every launch of "
+                             "the step is a fused pass); algorithmic bytes = read+write of the state"},
         "e2e": {"value": world / (e_ms / 1e3), "unit": "circuit/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "ms_per_step": e_ms},
         "clocks": clocks,
@@ -237,39 +241,57 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
+def _time_runs(s, arr, warm=4, reps=3):
+    import torch
+    stream = torch.cuda.ExternalStream(s.stream)
+    with torch.cuda.stream(stream):
+        for _ in range(warm):  # >= 4: JIT on the 2nd use, graphs after; QFT relabels alternate 2 plans
+            s.run(arr)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            s.run(arr)
+        b.record(stream)
+        torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 def sweep(args, local_rank):
-    """Extra single-GPU measurements reported beside the main line: per-gate
-    HBM GB/s at n=30 and fused-pass GB/s for QFT-30 (HBM regime)."""
+    """Single-GPU measurements beside the main line (BASELINE metric: circuit
+    time vs qubits; per-gate HBM GB/s vs peak; fused-pass GB/s)."""
     import torch
     import paper_2303_00123_b200 as qc
     import qcgen
-    res = {}
+    res = {"circuit_ms_vs_qubits": {}, "fused_pass": {}, "per_gate_n30": {}}
     peak, _ = load_peaks()
+    plan = [("qft", "c128", (16, 20, 24, 28, 30)), ("qft", "c64", (20, 26, 30)),
+            ("tfxy", "c128", (16, 20, 24, 28))]
+    for fam, prec, ns in plan:
+        key = f"{fam}_{prec}" + ("_S10" if fam == "tfxy" else "")
+        res["circuit_ms_vs_qubits"][key] = {}
+        for n in ns:
+            ops = qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, 10)
+            s = qc.State(n, prec, device=local_rank)
+            s.init_random(1)
+            t = _time_runs(s, qc.encode_ops(ops))
+            inf = s.info()
+            sb = (16 if prec == "c128" else 8) << n
+            entry = {"ms": round(t, 4), "gates": len(ops), "passes": inf["last_passes"],
+                     "jit": inf["last_jit"]}
+            if n >= 28:
+                gbps = 2 * sb * inf["last_passes"] / (t / 1e3) / 1e9
+                entry["fused_pass_GBps"] = round(gbps, 1)
+                entry["fused_pass_frac_of_measured_hbm"] = round(gbps / peak, 4)
+                res["fused_pass"][f"{fam}{n}_{prec}"] = entry["fused_pass_GBps"]
+            res["circuit_ms_vs_qubits"][key][str(n)] = entry
+            s.close()
+            torch.cuda.empty_cache()
     for prec in ("c128", "c64"):
         n = 30
         sb = (16 if prec == "c128" else 8) << n
         s = qc.State(n, prec, device=local_rank)
-        stream = torch.cuda.ExternalStream(s.stream)
         s.init_random(1)
-        ops = qcgen.qft(n)
-        arr = qc.encode_ops(ops)
-        with torch.cuda.stream(stream):
-            for _ in range(2):
-                s.run(arr)
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 3
-            a.record(stream)
-            for _ in range(reps):
-                s.run(arr)
-            b.record(stream)
-            torch.cuda.synchronize()
-        t = a.elapsed_time(b) / reps
-        passes = s.info()["last_passes"]
-        gbps = 2 * sb * passes / (t / 1e3) / 1e9
-        res[f"qft30_{prec}"] = {"ms": t, "passes": passes, "fused_pass_GBps": gbps,
-                                "frac_of_measured_hbm": gbps / peak}
-        # per-gate (unfused) GB/s for a few gate classes and qubit positions
         s.set_option("fusion", 0)
         s.set_option("relabel_swap", 0)
         pg = {}
@@ -280,18 +302,11 @@ def sweep(args, local_rank):
                                       ("SWAP", (1, 28), None, sb), ("U2", (7, 22), "U", 2 * sb)):
             g = qcgen.Op(name, qs, theta=arg if isinstance(arg, float) else None,
                          matrix=qcgen.random_unitary(4, np.random.default_rng(0)) if arg == "U" else None)
-            ga = qc.encode_ops([g])
-            with torch.cuda.stream(stream):
-                s.run(ga)
-                torch.cuda.synchronize()
-                a.record(stream)
-                for _ in range(5):
-                    s.run(ga)
-                b.record(stream)
-                torch.cuda.synchronize()
-            tg = a.elapsed_time(b) / 5
-            pg[f"{name}{list(qs)}"] = {"ms": round(tg, 4), "GBps": round(nbytes / (tg / 1e3) / 1e9, 1)}
-        res[f"per_gate_n30_{prec}"] = pg
+            tg = _time_runs(s, qc.encode_ops([g]), warm=1, reps=5)
+            gb = nbytes / (tg / 1e3) / 1e9
+            pg[f"{name}{list(qs)}"] = {"ms": round(tg, 4), "GBps": round(gb, 1),
+                                       "frac_of_measured_hbm": round(gb / peak, 4)}
+        res["per_gate_n30"][prec] = pg
         s.close()
         torch.cuda.empty_cache()
     return res
@@ -324,7 +339,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+    args.warmup = max(args.warmup, 5)  # JIT on 2nd use + graph capture; QFT relabels alternate plans
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
