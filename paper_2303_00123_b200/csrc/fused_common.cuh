@@ -335,6 +335,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   p += Body::smem_bytes(pd);
   uint64_t* full = reinterpret_cast<uint64_t*>(p);
   uint64_t* empty = full + NBUF;
+  volatile uint32_t* buf_tile = reinterpret_cast<volatile uint32_t*>(empty + NBUF);  // tile tag per buffer
   const int tid = threadIdx.x;
 
   body.setup(extra, pd);
@@ -347,6 +348,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     for (int b = 0; b < NBUF; ++b) {
       qc_mbar_init(&full[b], 1);
       qc_mbar_init(&empty[b], kGroupThreads);
+      buf_tile[b] = 0xffffffffu;
     }
     qc_fence_mbar_init();
   }
@@ -383,7 +385,10 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
       }
       if (i < my_n) {
         const uint64_t base = qc_tile_base(pd, blockIdx.x + i * gridDim.x);
-        if (lane == 0) qc_mbar_arrive_expect_tx(&full[b], tile_bytes);
+        if (lane == 0) {
+          buf_tile[b] = (uint32_t)i;  // full[b]'s pending phase now belongs to tile i
+          qc_mbar_arrive_expect_tx(&full[b], tile_bytes);
+        }
         __syncwarp();
         if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)
@@ -408,6 +413,10 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     const int par = (int)(i % kWSlots);
     const uint64_t tbase = qc_tile_base(pd, blockIdx.x + i * gridDim.x);
     body.prologue(tbase, par);
+    if (kGroups > 1 && NBUF % kGroups) {
+      // wait until the producer has claimed buffer b for this tile (see fused_types.h)
+      while (buf_tile[b] != (uint32_t)i) __nanosleep(64);
+    }
     qc_mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1ull));
     body.tile(bufs + (size_t)b * buf_amps, tbase, par);
     qc_fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
@@ -421,7 +430,7 @@ __host__ __device__ inline size_t qc_pipeline_smem(int k, int rb, int pshift, in
   const size_t PAD = kPadBytes / sizeof(C);
   const size_t nrows = (size_t)1 << (k - rb);
   const size_t buf_amps = ((size_t)1 << k) + (((size_t)1 << k) >> pshift) * PAD;
-  return (size_t)nbuf * buf_amps * sizeof(C) + nrows * 8 + 2 * (size_t)nbuf * 8;
+  return (size_t)nbuf * buf_amps * sizeof(C) + nrows * 8 + 2 * (size_t)nbuf * 8 + (size_t)nbuf * 4;
 }
 
 }  // namespace qc

@@ -19,10 +19,14 @@ constexpr int kSlots = 1 << kSlotBits;
 constexpr int kComputeWarps = 8;      // fused kernel: 8 compute warps ...
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kFusedThreads = kComputeThreads + 32;  // ... + 1 TMA producer warp
-// Two groups (alternate tiles) deadlocked intermittently under stress at
-// n=30 (DESIGN "open issues"); one group is the validated default.
+// Compute warps form kGroups groups that take alternate tiles.  With NBUF not
+// a multiple of kGroups a buffer's consecutive tiles go to different groups,
+// and a group running ahead could wait for phase p+1 of a buffer whose phase
+// p is still pending -- a parity wait would then match phase p-1.  The
+// producer therefore publishes a per-buffer tile tag, and consumers wait for
+// their tile's tag before the parity wait (qc_fused_pipeline).
 #ifndef QC_GROUPS
-#define QC_GROUPS 1
+#define QC_GROUPS 2
 #endif
 constexpr int kGroups = QC_GROUPS;    // compute warps form groups working on alternate tiles
 constexpr int kGroupThreads = kComputeThreads / kGroups;

@@ -233,7 +233,7 @@ size_t smem_for(const PassDesc& pd, int nbuf) {
 
 template <typename T>
 int pick_nbuf(const PassDesc& pd) {
-  for (int nb = 3; nb >= 2; --nb)  // >= 2: one buffer per compute group
+  for (int nb = 4; nb >= kGroups; --nb)
     if (smem_for<T>(pd, nb) <= kMaxSmem) return nb;
   return 0;
 }
@@ -248,6 +248,9 @@ int configure_t() {
                            (int)kMaxSmem);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(fused_pass_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kMaxSmem);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(fused_pass_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)kMaxSmem);
   return (int)e;
 }
@@ -264,6 +267,7 @@ int launch_t(void* state, const PassDesc& pd, const void* d_blob, const QcTmap& 
   C* s = reinterpret_cast<C*>(state);
   auto blob = reinterpret_cast<const uint8_t*>(d_blob);
   switch (nb) {
+    case 4: fused_pass_kernel<T, 4><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm); break;
     case 3: fused_pass_kernel<T, 3><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm); break;
     case 2: fused_pass_kernel<T, 2><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm); break;
     default: fused_pass_kernel<T, 1><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm); break;
