@@ -125,10 +125,38 @@ typedef struct qc_info {
     int32_t tile_bits;        /* k of the last fused run                        */
     int64_t last_blocks;      /* ops after block fusion (fused runs)            */
     int32_t last_jit;         /* 1 if the last run used NVRTC-specialised passes */
-    int32_t reserved;
+    int32_t world;            /* ranks the state is sharded over (1: not sharded) */
+    int32_t rank;             /* this rank                                       */
+    int32_t n_local;          /* qubits per shard (n - log2 world)               */
+    int32_t sharding;         /* 0 single GPU, 1 loopback (all shards here), 2 NCCL */
+    int64_t last_exchanges;   /* qubit-swap exchanges in the last run            */
 } qc_info;
 
 /* ---------------------------------------------------------------- lifetime */
+
+/* Sharded states (north star: shard the vector across B200s by
+ * its top log2(P) qubits, remap global<->local qubits by NCCL pairwise
+ * send/recv).  A state over P = 2^p ranks keeps 2^(n-p) amplitudes per rank;
+ * physical bits >= n-p are rank bits.  Gates whose non-diagonal targets are
+ * local run fused on each shard (rank-bit controls and diagonal bits are
+ * per-rank constants); a non-diagonal target on a rank bit triggers a
+ * qubit-swap exchange with the partner rank (half a shard per direction).
+ * Every rank must make the same calls with the same arguments (collective). */
+
+/* 128-byte NCCL unique id for qc_state_create_dist (call on one rank, then
+ * broadcast, e.g. over torch.distributed). */
+qc_status qc_nccl_unique_id(void* out128);
+
+/* One process per GPU: this rank's shard of an n-qubit state over `world`
+ * ranks (power of two), initialised to |0...0>; creates an NCCL communicator
+ * from `nccl_unique_id` (collective).  n - log2(world) >= 8. */
+qc_status qc_state_create_dist(int n, qc_precision p, int rank, int world,
+                               const void* nccl_unique_id, qc_state** out);
+
+/* All `world` shards in ONE process and ONE device buffer (2^n amplitudes):
+ * the sharded schedule and exchange arithmetic run exactly as with NCCL but
+ * exchanges are device swaps of the same runs.  For validation on one GPU. */
+qc_status qc_state_create_loopback(int n, qc_precision p, int world, qc_state** out);
 
 /* Allocate an n-qubit state on the current CUDA device, initialised to |0...0>,
  * with its own non-blocking stream.  1 <= n <= 40.  Returns NULL on error
@@ -177,7 +205,9 @@ qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops);
 /* ------------------------------------------------------------------ I/O */
 
 /* Copy canonical amplitudes [first, first+count) to host memory (count*s
- * bytes).  Blocks.  Undoes any pending relabel on the fly (gather kernel). */
+ * bytes).  Blocks.  Undoes any pending relabel on the fly (gather kernel).
+ * NCCL-sharded states: the layout must be canonical (qc_state_canonicalize)
+ * and the range inside this rank's shard [rank*2^(n-p), (rank+1)*2^(n-p)). */
 qc_status qc_state_read(qc_state* s, uint64_t first, uint64_t count, void* host_dst);
 
 /* Write canonical amplitudes [first, first+count) from host memory.  Blocks

@@ -34,6 +34,20 @@ qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops,
                         int row_bits, int block_fusion, int compile_jit, qc_plan_stats* out,
                         char* errbuf, size_t errlen);
 
+/* Sharded-state exchange arithmetic (host only): the runs of local indices
+ * (offset, count in amplitudes) that rank `rank` sends to -- and receives
+ * from -- `partner` when rank bit g is swapped with local bit l (n_loc local
+ * qubits).  Returns the run count in n_runs (fills at most max_runs). */
+qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, int* partner, uint64_t* offsets,
+                                 uint64_t* counts, int max_runs, int* n_runs);
+
+/* The sharded schedule qc_run_circuit would execute from the canonical
+ * layout (host only, deterministic): steps[4*i..] = (kind, g, l, gates) with
+ * kind 0 = fused local segment of `gates` gates, 1 = exchange of rank bit g
+ * with local bit l.  layout_out (n ints, may be NULL) = final layout. */
+qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
+                                 int* steps, int max_steps, int* n_steps, int* layout_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,6 +2,7 @@
 // launching, I/O.  Host code only (kernels live in kernels_*.cu).
 #include <cuda_runtime.h>
 
+#include <bit>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -12,11 +13,12 @@
 #include <vector>
 
 #include "qc_internal.h"
+#include "state.h"
 #include "../../include/qc_debug.h"
 
 using namespace qc;
 
-namespace {
+namespace qc {
 
 thread_local std::string g_err;
 
@@ -34,63 +36,6 @@ const int kArity[16] = {1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 1, 2, 2, 3};
 const int kNctrl[16] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 0, 2};
 const char* kName[16] = {"H", "X", "Y", "Z", "P", "RX", "RY", "RZ",
                          "CNOT", "CZ", "CP", "SWAP", "U1", "CU1", "U2", "CCX"};
-
-struct PlanEntry {
-  std::vector<qc_gate> ops;          // exact copy (collision check)
-  std::vector<int> layout_in, layout_out;
-  std::vector<PassDesc> passes;
-  void* d_blob = nullptr;
-  int64_t fused_gates = 0;
-  std::shared_ptr<FusedPlan> ir;     // kept for JIT specialisation
-  std::vector<JitKernel> jit;
-  int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
-  QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
-  bool dbl = true;
-  int64_t relabels = 0;
-  int uses = 0;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  int ctas = 0;
-  int tile_bits = 0;
-  ~PlanEntry() {
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    if (d_blob) cudaFree(d_blob);
-  }
-};
-
-}  // namespace
-
-struct qc_state {
-  int n = 0;
-  qc_precision prec = QC_COMPLEX128;
-  bool dbl = true;
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  void* d = nullptr;
-  bool own_mem = false;
-  size_t bytes = 0;
-  int layout[64];
-  bool failed = false;
-  // options
-  int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0, block_fusion = 1, jit = 1;
-  int row_bits = 0, tma_mode = 0;
-  std::string jit_error;
-  // stats
-  int64_t last_gates = 0, last_passes = 0, last_launches = 0, last_relabels = 0;
-  int last_graph = 0, last_k = 0;
-  int64_t last_blocks = 0;
-  int last_jit = 0;
-  // plan cache
-  std::unordered_map<uint64_t, std::unique_ptr<PlanEntry>> plans;
-  cudaStream_t cap_stream = nullptr;
-  void* d_stage = nullptr;
-  size_t stage_bytes = 0;
-  double* d_partial = nullptr;
-};
-
-namespace {
 
 size_t amp_bytes(const qc_state* s) { return s->dbl ? 16 : 8; }
 
@@ -204,16 +149,55 @@ uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint6
   return h;
 }
 
-// Build (or fetch) the fused plan for this op list and the current layout.
-qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
-  const int n = s->n;
+void plan_geometry(const qc_state* s, int n_plan, int* k_out, int* rb_out, int* ctas_out) {
   int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
   if (s->dbl && k > 12) k = 12;  // two 2^k tiles (one per compute group) must fit in smem
-  if (k > n) k = n;
+  if (k > n_plan) k = n_plan;
   int rb = s->row_bits ? s->row_bits : (s->dbl ? 5 : 6);
   if (rb > k - 2) rb = k - 2;
   if (rb < 1) rb = 1;
-  const int ctas = s->ctas ? s->ctas : sm_count();
+  *k_out = k;
+  *rb_out = rb;
+  *ctas_out = s->ctas ? s->ctas : sm_count();
+}
+
+// Fuse + plan + pack + upload lowered gates over n_plan local bits (bits at or
+// above n_plan -- the rank bits of a sharded state -- may appear only as
+// controls / diagonal bits).  `tmap_base` / `tmap_bits`: the buffer and index
+// width the row tensor map spans.
+qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
+                            PlanEntry* e, void* tmap_base, int tmap_bits) {
+  int k, rb, ctas;
+  plan_geometry(s, n_plan, &k, &rb, &ctas);
+  e->ctas = ctas;
+  e->tile_bits = k;
+  std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
+  e->fused_gates = (int64_t)blocks.size();
+  if (blocks.empty()) return QC_OK;
+  FusedPlan fp = plan_fused(n_plan, k, rb, blocks);
+  if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
+  const bool g4 = s->tma_mode == 0 && make_row_tmap(tmap_base ? tmap_base : s->d, tmap_bits ? tmap_bits : n_plan, rb,
+                                                     s->dbl, &e->tmap);
+  for (auto& p : fp.passes) {
+    p.desc.g4 = g4 ? 1 : 0;
+    p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
+  }
+  std::vector<uint8_t> blob = pack_plan(fp, s->dbl);
+  for (auto& p : fp.passes) e->passes.push_back(p.desc);
+  e->dbl = s->dbl;
+  e->ir = std::make_shared<FusedPlan>(std::move(fp));
+  cudaError_t ce = cudaMalloc(&e->d_blob, blob.size());
+  if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
+  ce = cudaMemcpy(e->d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
+  return QC_OK;
+}
+
+// Build (or fetch) the fused plan for this op list and the current layout.
+qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
+  const int n = s->n;
+  int k, rb, ctas;
+  plan_geometry(s, n, &k, &rb, &ctas);
   const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
                         ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)(s->jit == 2) << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^
                         ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
@@ -230,8 +214,6 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   auto e = std::make_unique<PlanEntry>();
   e->ops.assign(ops, ops + n_ops);
   e->layout_in.assign(s->layout, s->layout + n);
-  e->ctas = ctas;
-  e->tile_bits = k;
   // lower in order, applying SWAP relabels to a running layout
   int lay[64];
   std::memcpy(lay, s->layout, sizeof(int) * n);
@@ -249,25 +231,8 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   }
   e->layout_out.assign(lay, lay + n);
   if (!gates.empty()) {
-    std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates) : gates;
-    e->fused_gates = (int64_t)blocks.size();
-    if (!blocks.empty()) {
-      FusedPlan fp = plan_fused(n, k, rb, blocks);
-      if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
-      const bool g4 = s->tma_mode == 0 && make_row_tmap(s->d, n, rb, s->dbl, &e->tmap);
-      for (auto& p : fp.passes) {
-        p.desc.g4 = g4 ? 1 : 0;
-        p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
-      }
-      std::vector<uint8_t> blob = pack_plan(fp, s->dbl);
-      for (auto& p : fp.passes) e->passes.push_back(p.desc);
-      e->dbl = s->dbl;
-      e->ir = std::make_shared<FusedPlan>(std::move(fp));
-      cudaError_t ce = cudaMalloc(&e->d_blob, blob.size());
-      if (ce != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "plan upload: %s", cudaGetErrorString(ce));
-      ce = cudaMemcpy(e->d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
-      if (ce != cudaSuccess) return cuda_fail(s, ce, "plan upload");
-    }
+    const qc_status bs = build_fused_entry(s, gates, n, ~0ull, e.get());
+    if (bs != QC_OK) return bs;
   }
   PlanEntry* raw = e.get();
   if (s->plans.size() > 64) s->plans.clear();
@@ -276,28 +241,24 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   return QC_OK;
 }
 
-int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) {
+// Launch every pass of a fused entry; rank_bits / addr_bits: see PassDesc.
+int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
+                  uint64_t addr_bits) {
   for (size_t i = 0; i < e->passes.size(); ++i) {
-    const PassDesc& pd = e->passes[i];
-    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], s->d, pd, e->tmap, e->ctas, st)
-                                      : launch_fused_pass(s->d, s->dbl, pd, e->d_blob, e->tmap, e->ctas, st);
+    PassDesc pd = e->passes[i];
+    pd.rank_bits = rank_bits;
+    pd.addr_bits = addr_bits;
+    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, e->tmap, e->ctas, st)
+                                      : launch_fused_pass(base, s->dbl, pd, e->d_blob, e->tmap, e->ctas, st);
     if (r) return r;
   }
   return 0;
 }
 
-qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
-  static bool configured[2] = {false, false};
-  if (!configured[s->dbl]) {
-    const int r = fused_configure(s->dbl);
-    if (r) return cuda_fail(s, r, "cudaFuncSetAttribute(fused)");
-    configured[s->dbl] = true;
-  }
-  PlanEntry* e = nullptr;
-  qc_status st = get_plan(s, ops, n_ops, &e);
-  if (st != QC_OK) return st;
-  e->uses++;
-  s->last_graph = 0;
+int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) { return enqueue_entry(s, e, st, s->d, 0, 0); }
+
+// NVRTC-specialise an entry according to the JIT policy (2nd use by default).
+qc_status maybe_jit(qc_state* s, PlanEntry* e) {
   if (e->jit_state == 0 && e->ir && (s->jit == 2 || (s->jit == 1 && e->uses >= 2))) {
     std::string err;
     if (jit_build(*e->ir, s->dbl, e->jit, err)) {
@@ -308,6 +269,31 @@ qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
       if (s->jit == 2) return fail(QC_ERR_UNSUPPORTED, "JIT specialisation failed: %s", err.c_str());
     }
   }
+  return QC_OK;
+}
+
+qc_status ensure_fused_configured(qc_state* s) {
+  static bool configured[2] = {false, false};  // per process (device attributes of our kernels)
+  if (!configured[s->dbl]) {
+    const int r = fused_configure(s->dbl);
+    if (r) return cuda_fail(s, r, "cudaFuncSetAttribute(fused)");
+    configured[s->dbl] = true;
+  }
+  return QC_OK;
+}
+
+qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  {
+    const qc_status c = ensure_fused_configured(s);
+    if (c != QC_OK) return c;
+  }
+  PlanEntry* e = nullptr;
+  qc_status st = get_plan(s, ops, n_ops, &e);
+  if (st != QC_OK) return st;
+  e->uses++;
+  s->last_graph = 0;
+  st = maybe_jit(s, e);
+  if (st != QC_OK) return st;
   int r = 0;
   if (s->use_graph && e->uses >= 2 && !e->passes.empty()) {
     if (!e->exec) {
@@ -375,7 +361,8 @@ qc_status ensure_stage(qc_state* s, size_t bytes) {
   return QC_OK;
 }
 
-qc_status new_state(int n, qc_precision p, int device, void* stream, void* dev_ptr, qc_state** out) {
+qc_status new_state(int n, qc_precision p, int device, void* stream, void* dev_ptr, qc_state** out,
+                    int dist = 0, int world = 1, int rank = 0) {
   if (!out) return fail(QC_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (n < 1 || n > kMaxQubits) return fail(QC_ERR_INVALID_ARG, "n=%d outside [1,%d]", n, kMaxQubits);
@@ -391,7 +378,12 @@ qc_status new_state(int n, qc_precision p, int device, void* stream, void* dev_p
   s->prec = p;
   s->dbl = (p == QC_COMPLEX128);
   s->device = device;
-  s->bytes = (size_t)(s->dbl ? 16 : 8) << n;
+  s->dist = dist;
+  s->world = world;
+  s->rank = rank;
+  s->n_loc = n - std::countr_zero((unsigned)world);
+  // loopback keeps every rank's shard in one buffer; NCCL keeps the local shard
+  s->bytes = (size_t)(s->dbl ? 16 : 8) << (dist == 2 ? s->n_loc : n);
   canonical_layout(s.get());
   if (stream) {
     s->stream = reinterpret_cast<cudaStream_t>(stream);
@@ -413,7 +405,7 @@ qc_status new_state(int n, qc_precision p, int device, void* stream, void* dev_p
                   cudaGetErrorString(e));
     }
     s->own_mem = true;
-    const int r = launch_init_basis(s->d, n, s->dbl, 0, s->stream);
+    const int r = (dist == 2) ? launch_init_basis(s->d, s->n_loc, s->dbl, 0, s->stream) : launch_init_basis(s->d, n, s->dbl, 0, s->stream);
     if (r) {
       cudaFree(s->d);
       if (s->own_stream) cudaStreamDestroy(s->stream);
@@ -449,11 +441,52 @@ qc_status qc_state_wrap(int n, qc_precision p, void* dev_ptr, void* cuda_stream,
   return new_state(n, p, -1, cuda_stream, dev_ptr, out);
 }
 
+qc_status qc_state_create_loopback(int n, qc_precision p, int world, qc_state** out) {
+  if (world < 2 || (world & (world - 1)) || world > 64)
+    return fail(QC_ERR_INVALID_ARG, "world must be a power of two in [2, 64]");
+  if (n - std::countr_zero((unsigned)world) < 8)
+    return fail(QC_ERR_INVALID_ARG, "each shard needs >= 8 local qubits");
+  return new_state(n, p, -1, nullptr, nullptr, out, 1, world, 0);
+}
+
+qc_status qc_nccl_unique_id(void* out128) {
+  if (!out128) return fail(QC_ERR_INVALID_ARG, "out is NULL");
+  return nccl_get_unique_id(out128);
+}
+
+qc_status qc_state_create_dist(int n, qc_precision p, int rank, int world, const void* nccl_unique_id,
+                               qc_state** out) {
+  if (!out) return fail(QC_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || (world & (world - 1)) || world > 64)
+    return fail(QC_ERR_INVALID_ARG, "world must be a power of two in [1, 64]");
+  if (rank < 0 || rank >= world) return fail(QC_ERR_INVALID_ARG, "rank out of range");
+  if (world == 1) return new_state(n, p, -1, nullptr, nullptr, out);
+  if (!nccl_unique_id) return fail(QC_ERR_INVALID_ARG, "nccl_unique_id is NULL");
+  if (n - std::countr_zero((unsigned)world) < 8)
+    return fail(QC_ERR_INVALID_ARG, "each shard needs >= 8 local qubits");
+  qc_state* s = nullptr;
+  qc_status st = new_state(n, p, -1, nullptr, nullptr, &s, 2, world, rank);
+  if (st != QC_OK) return st;
+  if (rank != 0) {  // |0...0> lives on rank 0 only
+    cudaMemsetAsync(s->d, 0, s->bytes, s->stream);
+  }
+  st = nccl_create_comm(s, nccl_unique_id);
+  if (st != QC_OK) {
+    qc_state_destroy(s);
+    return st;
+  }
+  *out = s;
+  return QC_OK;
+}
+
 void qc_state_destroy(qc_state* s) {
   if (!s) return;
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
   s->plans.clear();
+  dist_release(s);
+  if (s->d_xstage) cudaFree(s->d_xstage);
   if (s->own_mem && s->d) cudaFree(s->d);
   if (s->d_stage) cudaFree(s->d_stage);
   if (s->d_partial) cudaFree(s->d_partial);
@@ -467,6 +500,22 @@ qc_status qc_state_init_basis(qc_state* s, uint64_t k) {
   if (st != QC_OK) return st;
   if (k >> s->n) return fail(QC_ERR_INVALID_ARG, "basis index %llu >= 2^%d", (unsigned long long)k, s->n);
   canonical_layout(s);
+  if (s->dist == 2) {  // canonical: rank r holds [r << n_loc, (r+1) << n_loc)
+    const uint64_t nl = 1ull << s->n_loc;
+    cudaError_t e = cudaMemsetAsync(s->d, 0, s->bytes, s->stream);
+    if (e != cudaSuccess) return cuda_fail(s, e, "init_basis");
+    if ((k / nl) == (uint64_t)s->rank) {
+      const int r = launch_init_basis(s->d, 0, s->dbl, 0, s->stream);  // n=0: sets element 0 only... see below
+      (void)r;
+      double one[2] = {1.0, 0.0};
+      float onef[2] = {1.0f, 0.0f};
+      e = cudaMemcpyAsync((char*)s->d + (k % nl) * amp_bytes(s), s->dbl ? (void*)one : (void*)onef,
+                          amp_bytes(s), cudaMemcpyHostToDevice, s->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+      if (e != cudaSuccess) return cuda_fail(s, e, "init_basis");
+    }
+    return QC_OK;
+  }
   const int r = launch_init_basis(s->d, s->n, s->dbl, k, s->stream);
   if (r) return cuda_fail(s, r, "init_basis");
   return QC_OK;
@@ -476,7 +525,9 @@ qc_status qc_state_init_random(qc_state* s, uint64_t seed) {
   qc_status st = check_state(s);
   if (st != QC_OK) return st;
   canonical_layout(s);
-  const int r = launch_init_random(s->d, s->n, s->dbl, seed, s->stream);
+  const int r = (s->dist == 2) ? launch_init_random(s->d, s->n, s->dbl, seed, s->stream,
+                                                   (uint64_t)s->rank << s->n_loc, 1ull << s->n_loc)
+                               : launch_init_random(s->d, s->n, s->dbl, seed, s->stream);
   if (r) return cuda_fail(s, r, "init_random");
   return QC_OK;
 }
@@ -498,6 +549,7 @@ qc_status qc_apply_gate(qc_state* s, qc_op op, const int* qubits, const double* 
   for (int i = 0; i < nm; ++i) g.m[i] = matrix[i];
   st = validate_gate(s->n, g, 0);
   if (st != QC_OK) return st;
+  if (s->dist) return run_dist(s, &g, 1);
   return run_unfused(s, &g, 1);
 }
 
@@ -514,6 +566,7 @@ qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops) {
     s->last_passes = s->last_launches = s->last_relabels = 0;
     return QC_OK;
   }
+  if (s->dist) return run_dist(s, ops, n_ops);  // sharded: fused segments + exchanges
   if (s->fusion && s->n >= kSlotBits) return run_fused(s, ops, n_ops);
   return run_unfused(s, ops, n_ops);
 }
@@ -535,6 +588,15 @@ qc_status qc_state_read(qc_state* s, uint64_t first, uint64_t count, void* host_
     return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
                 (unsigned long long)count, s->n);
   if (!count) return QC_OK;
+  if (s->dist == 2) {  // NCCL shard: canonical layout, range inside this rank's shard
+    const uint64_t nl = 1ull << s->n_loc, lo = (uint64_t)s->rank * nl;
+    if (!layout_is_canonical(s))
+      return fail(QC_ERR_UNSUPPORTED, "sharded state: call qc_state_canonicalize (collective) first");
+    if (first < lo || first + count > lo + nl)
+      return fail(QC_ERR_INVALID_ARG, "sharded state: rank %d holds [%llu, %llu)", s->rank,
+                  (unsigned long long)lo, (unsigned long long)(lo + nl));
+    first -= lo;
+  }
   const size_t ab = amp_bytes(s);
   cudaError_t e;
   if (layout_is_canonical(s)) {
@@ -566,6 +628,15 @@ qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void
     return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
                 (unsigned long long)count, s->n);
   if (!count) return QC_OK;
+  if (s->dist == 2) {  // NCCL shard: canonical layout, range inside this rank's shard
+    const uint64_t nl = 1ull << s->n_loc, lo = (uint64_t)s->rank * nl;
+    if (!layout_is_canonical(s))
+      return fail(QC_ERR_UNSUPPORTED, "sharded state: call qc_state_canonicalize (collective) first");
+    if (first < lo || first + count > lo + nl)
+      return fail(QC_ERR_INVALID_ARG, "sharded state: rank %d holds [%llu, %llu)", s->rank,
+                  (unsigned long long)lo, (unsigned long long)(lo + nl));
+    first -= lo;
+  }
   const size_t ab = amp_bytes(s);
   cudaError_t e;
   if (layout_is_canonical(s)) {
@@ -591,6 +662,7 @@ qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void
 qc_status qc_state_canonicalize(qc_state* s) {
   qc_status st = check_state(s);
   if (st != QC_OK) return st;
+  if (s->dist) return dist_canonicalize(s);
   for (int q = 0; q < s->n; ++q) {
     const int want = s->n - 1 - q;
     if (s->layout[q] == want) continue;
@@ -618,7 +690,7 @@ qc_status qc_state_norm2(qc_state* s, double* out) {
     cudaError_t e = cudaMalloc(&s->d_partial, nb * sizeof(double));
     if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "norm partials: %s", cudaGetErrorString(e));
   }
-  const int r = launch_norm2(s->d, s->n, s->dbl, s->d_partial, nb, s->stream);
+  const int r = launch_norm2(s->d, s->dist == 2 ? s->n_loc : s->n, s->dbl, s->d_partial, nb, s->stream);
   if (r) return cuda_fail(s, r, "norm2");
   std::vector<double> h(nb);
   cudaError_t e = cudaMemcpyAsync(h.data(), s->d_partial, nb * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
@@ -627,6 +699,10 @@ qc_status qc_state_norm2(qc_state* s, double* out) {
   if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
   double t = 0;
   for (double v : h) t += v;
+  if (s->dist == 2) {
+    st = nccl_allreduce_sum(s, &t);
+    if (st != QC_OK) return st;
+  }
   *out = t;
   return QC_OK;
 }
@@ -680,6 +756,11 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
   out->tile_bits = s->last_k;
   out->last_blocks = s->last_blocks;
   out->last_jit = s->last_jit;
+  out->world = s->world;
+  out->rank = s->rank;
+  out->n_local = s->dist ? s->n_loc : s->n;
+  out->sharding = s->dist;
+  out->last_exchanges = s->last_exchanges;
   return QC_OK;
 }
 
@@ -719,7 +800,7 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   }
   out->gates = (int64_t)n_ops;
   out->tile_bits = k;
-  std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates) : gates;
+  std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates, ~0ull) : gates;
   out->blocks = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
   FusedPlan fp = plan_fused(n, k, rb, blocks);
@@ -738,5 +819,33 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
     if (!jit_compile_only(fp, dbl, compiled, e)) return err(QC_ERR_UNSUPPORTED, e);
     out->jit_compiled = compiled;
   }
+  return QC_OK;
+}
+
+extern "C" qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, int* partner, uint64_t* offsets,
+                                           uint64_t* counts, int max_runs, int* n_runs) {
+  if (!partner || !n_runs || g < n_loc || l < 0 || l >= n_loc) return fail(QC_ERR_INVALID_ARG, "bad arguments");
+  const auto runs = exchange_runs(n_loc, rank, g, l, partner);
+  *n_runs = (int)runs.size();
+  for (int i = 0; i < (int)runs.size() && i < max_runs; ++i) {
+    if (offsets) offsets[i] = runs[i].offset;
+    if (counts) counts[i] = runs[i].count;
+  }
+  return QC_OK;
+}
+
+extern "C" qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
+                                           int* steps, int max_steps, int* n_steps, int* layout_out) {
+  if (!n_steps || world < 2 || (world & (world - 1))) return fail(QC_ERR_INVALID_ARG, "bad arguments");
+  for (size_t i = 0; i < n_ops; ++i) {
+    const qc_status st = validate_gate(n, ops[i], i);
+    if (st != QC_OK) return st;
+  }
+  std::vector<int> out, lay;
+  const qc_status st = dist_schedule_dry(n, world, relabel, ops, n_ops, out, lay);
+  if (st != QC_OK) return st;
+  *n_steps = (int)out.size() / 4;
+  if (steps) std::memcpy(steps, out.data(), sizeof(int) * std::min<size_t>(out.size(), (size_t)max_steps * 4));
+  if (layout_out) std::memcpy(layout_out, lay.data(), sizeof(int) * lay.size());
   return QC_OK;
 }

@@ -1,0 +1,489 @@
+// dist.cu -- the sharded state (north star "shards the vector
+// across the B200s by its top log2(P) qubits and remaps global to local qubits
+// through NCCL pairwise send/recv").
+//
+// A state of n qubits over P = 2^p ranks keeps 2^{n_loc} = 2^{n-p} amplitudes
+// per rank; physical bits >= n_loc are rank bits.  Every gate is still the
+// eq:kron operator; on a shard:
+//   * a gate whose non-diagonal targets are local runs in the fused engine on
+//     the shard; controls / diagonal bits on rank bits are per-rank constants
+//     (PassDesc::rank_bits is OR-ed into every tile's base index);
+//   * a non-diagonal target on a rank bit g first swaps g with a local bit l
+//     ("qubit-swap exchange"): rank r and its partner r ^ 2^{g-n_loc} trade
+//     the local half where bit l != their bit g; afterwards the logical qubits
+//     at g and l have exchanged physical positions (layout update).
+// The schedule is computed identically on every rank (host, deterministic):
+// the local victim is the qubit whose next non-diagonal use is farthest away
+// (Belady); if it is not already at the exchange slot l = n_loc-1 a physical
+// SWAP of the two local bits is inserted into the preceding fused segment,
+// so every exchange moves ONE contiguous half shard per direction.
+//
+// Backends: NCCL (one process per GPU; libnccl dlopen'ed, grouped chunked
+// ncclSend/ncclRecv through a staging buffer, stream-ordered) and loopback
+// (all P shards of one process in one buffer on one GPU; the exchange swaps
+// the same runs in place) -- the latter exercises the whole sharded path on a
+// single GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <bit>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "state.h"
+
+qc_state::~qc_state() {}
+
+namespace qc {
+
+struct DistPlan {
+  std::vector<qc_gate> ops;
+  std::vector<int> layout_in, layout_out;
+  struct Step {
+    int kind = 0;  // 0: fused local segment, 1: exchange
+    int g = -1, l = -1;
+    std::unique_ptr<PlanEntry> seg;
+  };
+  std::vector<Step> steps;
+  int64_t exchanges = 0, relabels = 0, passes = 0;
+  int uses = 0;
+};
+
+struct DistCache {
+  std::unordered_map<uint64_t, std::unique_ptr<DistPlan>> plans;
+};
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL
+typedef struct {
+  char internal[128];
+} QcNcclId;
+enum { kNcclUint8 = 1, kNcclFloat64 = 8, kNcclSum = 0 };
+struct Nccl {
+  int (*get_unique_id)(QcNcclId*) = nullptr;
+  int (*comm_init_rank)(void**, int, QcNcclId, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool ok = false;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("QC_NCCL_LIB");
+    const char* names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* nm : names)
+      if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return;
+#define QC_NSYM(f, s) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, s))
+    QC_NSYM(get_unique_id, "ncclGetUniqueId");
+    QC_NSYM(comm_init_rank, "ncclCommInitRank");
+    QC_NSYM(comm_destroy, "ncclCommDestroy");
+    QC_NSYM(send, "ncclSend");
+    QC_NSYM(recv, "ncclRecv");
+    QC_NSYM(group_start, "ncclGroupStart");
+    QC_NSYM(group_end, "ncclGroupEnd");
+    QC_NSYM(all_reduce, "ncclAllReduce");
+    QC_NSYM(error_string, "ncclGetErrorString");
+#undef QC_NSYM
+    n.ok = n.get_unique_id && n.comm_init_rank && n.comm_destroy && n.send && n.recv && n.group_start &&
+           n.group_end && n.all_reduce;
+  });
+  return n;
+}
+
+qc_status nccl_fail(qc_state* s, int r, const char* what) {
+  if (s) s->failed = true;
+  return fail(QC_ERR_NCCL, "%s: %s", what, nccl().error_string ? nccl().error_string(r) : "nccl error");
+}
+
+// non-diagonal target qubits of a (logical) op
+uint32_t nondiag_qubits_mask(const qc_gate& g, int n) {
+  (void)n;
+  switch (g.op) {
+    case QC_Z: case QC_P: case QC_RZ: case QC_CZ: case QC_CP: return 0;
+    case QC_SWAP: case QC_U2: return (1u << g.qubits[0]) | (1u << g.qubits[1]);
+    default: return 1u << g.qubits[kNctrl[g.op]];
+  }
+}
+
+}  // namespace
+
+std::vector<ExchangeRun> exchange_runs(int n_loc, int rank, int g, int l, int* partner) {
+  const int gb = g - n_loc;
+  if (partner) *partner = rank ^ (1 << gb);
+  const uint64_t mybit = (uint64_t)((rank >> gb) & 1);
+  const uint64_t want = 1 - mybit;  // bit l of the local indices that are traded
+  std::vector<ExchangeRun> runs;
+  const uint64_t run = 1ull << l;
+  const uint64_t nruns = 1ull << (n_loc - 1 - l);
+  for (uint64_t k = 0; k < nruns; ++k) runs.push_back({k * 2 * run + want * run, run});
+  return runs;
+}
+
+qc_status nccl_create_comm(qc_state* s, const void* unique_id) {
+  Nccl& N = nccl();
+  if (!N.ok) return fail(QC_ERR_NCCL, "libnccl.so.2 not found (set QC_NCCL_LIB)");
+  QcNcclId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  const int r = N.comm_init_rank(&s->nccl_comm, s->world, id, s->rank);
+  if (r) return nccl_fail(s, r, "ncclCommInitRank");
+  return QC_OK;
+}
+
+qc_status nccl_get_unique_id(void* out128) {
+  Nccl& N = nccl();
+  if (!N.ok) return fail(QC_ERR_NCCL, "libnccl.so.2 not found (set QC_NCCL_LIB)");
+  QcNcclId id;
+  const int r = N.get_unique_id(&id);
+  if (r) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  std::memcpy(out128, &id, sizeof id);
+  return QC_OK;
+}
+
+void dist_release(qc_state* s) {
+  delete s->dcache;
+  s->dcache = nullptr;
+  nccl_destroy(s);
+}
+
+void nccl_destroy(qc_state* s) {
+  if (s->nccl_comm && nccl().ok) nccl().comm_destroy(s->nccl_comm);
+  s->nccl_comm = nullptr;
+}
+
+qc_status nccl_allreduce_sum(qc_state* s, double* host_value) {
+  Nccl& N = nccl();
+  double* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(double), s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaMallocAsync");
+  cudaMemcpyAsync(d, host_value, sizeof(double), cudaMemcpyHostToDevice, s->stream);
+  const int r = N.all_reduce(d, d, 1, kNcclFloat64, kNcclSum, s->nccl_comm, s->stream);
+  if (r) return nccl_fail(s, r, "ncclAllReduce");
+  cudaMemcpyAsync(host_value, d, sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  cudaFreeAsync(d, s->stream);
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  return QC_OK;
+}
+
+// Swap physical rank bit g with local bit l (stream-ordered).
+qc_status dist_exchange(qc_state* s, int g, int l) {
+  const size_t ab = s->dbl ? 16 : 8;
+  if (s->dist == 1) {  // loopback: rank r's shard is [r << n_loc, (r+1) << n_loc) of one buffer
+    for (int r = 0; r < s->world; ++r) {
+      int partner;
+      const auto mine = exchange_runs(s->n_loc, r, g, l, &partner);
+      if (partner < r) continue;  // each pair once
+      const auto theirs = exchange_runs(s->n_loc, partner, g, l, nullptr);
+      for (size_t k = 0; k < mine.size(); ++k) {
+        char* a = (char*)s->d + (((uint64_t)r << s->n_loc) + mine[k].offset) * ab;
+        char* b = (char*)s->d + (((uint64_t)partner << s->n_loc) + theirs[k].offset) * ab;
+        const int e = launch_swap_regions(a, b, mine[k].count * ab, s->stream);
+        if (e) return cuda_fail(s, e, "loopback exchange");
+      }
+    }
+    return QC_OK;
+  }
+  // NCCL: send my runs to the partner, receive its runs into the same places
+  Nccl& N = nccl();
+  int partner;
+  const auto runs = exchange_runs(s->n_loc, s->rank, g, l, &partner);
+  const size_t chunk_max = 256ull << 20;
+  if (s->xstage_bytes < chunk_max) {
+    if (s->d_xstage) cudaFree(s->d_xstage);
+    cudaError_t e = cudaMalloc(&s->d_xstage, chunk_max);
+    if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "exchange staging (%zu B)", chunk_max);
+    s->xstage_bytes = chunk_max;
+  }
+  for (const auto& run : runs) {
+    const size_t bytes = run.count * ab;
+    char* base = (char*)s->d + run.offset * ab;
+    for (size_t off = 0; off < bytes; off += chunk_max) {
+      const size_t m = std::min(chunk_max, bytes - off);
+      int r = N.group_start();
+      if (!r) r = N.send(base + off, m, kNcclUint8, partner, s->nccl_comm, s->stream);
+      if (!r) r = N.recv(s->d_xstage, m, kNcclUint8, partner, s->nccl_comm, s->stream);
+      const int r2 = N.group_end();
+      if (r || r2) return nccl_fail(s, r ? r : r2, "exchange send/recv");
+      cudaError_t e = cudaMemcpyAsync(base + off, s->d_xstage, m, cudaMemcpyDeviceToDevice, s->stream);
+      if (e != cudaSuccess) return cuda_fail(s, e, "exchange copy");
+    }
+  }
+  return QC_OK;
+}
+
+namespace {
+
+// Build the exchange / segment schedule for an op list from the state's layout.
+// dry_run: schedule only (no device work; segments record their gate count).
+qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPlan* P, bool dry_run = false) {
+  const int n = s->n, nl = s->n_loc;
+  const int L = nl - 1;  // exchange slot: the top local bit (one contiguous half per direction)
+  int lay[64], inv[64];
+  std::memcpy(lay, s->layout, sizeof(int) * n);
+  for (int q = 0; q < n; ++q) inv[lay[q]] = q;
+  // next non-diagonal use of each logical qubit after op i (Belady)
+  std::vector<std::vector<int>> uses(n);
+  for (size_t i = 0; i < n_ops; ++i) {
+    if (ops[i].op == QC_SWAP && s->relabel) continue;
+    const uint32_t m = nondiag_qubits_mask(ops[i], n);
+    for (int q = 0; q < n; ++q)
+      if (m & (1u << q)) uses[q].push_back((int)i);
+  }
+  auto next_use = [&](int q, size_t i) -> long {
+    auto it = std::upper_bound(uses[q].begin(), uses[q].end(), (int)i);
+    return it == uses[q].end() ? (long)1 << 40 : (long)*it;
+  };
+  std::vector<PGate> seg;
+  auto flush = [&]() -> qc_status {
+    if (seg.empty()) return QC_OK;
+    DistPlan::Step st;
+    st.kind = 0;
+    st.seg = std::make_unique<PlanEntry>();
+    if (dry_run) {
+      st.seg->fused_gates = (int64_t)seg.size();
+      P->steps.push_back(std::move(st));
+      seg.clear();
+      return QC_OK;
+    }
+    const uint64_t local_mask = (1ull << nl) - 1;
+    const qc_status r = build_fused_entry(s, seg, nl, local_mask, st.seg.get(), s->d,
+                                          s->dist == 1 ? n : nl);
+    if (r != QC_OK) return r;
+    P->passes += (int64_t)st.seg->passes.size();
+    P->steps.push_back(std::move(st));
+    seg.clear();
+    return QC_OK;
+  };
+  for (size_t i = 0; i < n_ops; ++i) {
+    const qc_gate& op = ops[i];
+    if (op.op == QC_SWAP && s->relabel) {
+      std::swap(lay[op.qubits[0]], lay[op.qubits[1]]);
+      inv[lay[op.qubits[0]]] = op.qubits[0];
+      inv[lay[op.qubits[1]]] = op.qubits[1];
+      P->relabels++;
+      continue;
+    }
+    const uint32_t nd = nondiag_qubits_mask(op, n);
+    uint32_t op_qubits = 0;
+    for (int t = 0; t < kArity[op.op]; ++t) op_qubits |= 1u << op.qubits[t];
+    for (int q = 0; q < n; ++q) {
+      if (!(nd & (1u << q)) || lay[q] < nl) continue;
+      // qubit q is non-diagonal and global: bring it to local bit L
+      const int g = lay[q];
+      int victim = -1;
+      long best = -1;
+      for (int p = 0; p < nl; ++p) {
+        const int vq = inv[p];
+        if (op_qubits & (1u << vq)) continue;  // must stay local for this op
+        const long nu = next_use(vq, i);
+        const long score = nu * 2 + (p == L ? 1 : 0);  // prefer the slot itself on ties
+        if (score > best) {
+          best = score;
+          victim = p;
+        }
+      }
+      if (victim < 0) return fail(QC_ERR_UNSUPPORTED, "no local qubit free for an exchange");
+      if (victim != L) {  // physical SWAP of two local bits, fused into the segment
+        PGate sw;
+        sw.kind = GK::SWAP2;
+        sw.t0 = std::max(victim, L);
+        sw.t1 = std::min(victim, L);
+        seg.push_back(sw);
+        const int qa = inv[victim], qb = inv[L];
+        std::swap(lay[qa], lay[qb]);
+        inv[lay[qa]] = qa;
+        inv[lay[qb]] = qb;
+      }
+      qc_status r = flush();
+      if (r != QC_OK) return r;
+      DistPlan::Step ex;
+      ex.kind = 1;
+      ex.g = g;
+      ex.l = L;
+      P->steps.push_back(std::move(ex));
+      P->exchanges++;
+      const int qg = inv[g], ql = inv[L];
+      std::swap(lay[qg], lay[ql]);
+      inv[lay[qg]] = qg;
+      inv[lay[ql]] = ql;
+    }
+    PGate pg = lower(op, lay);
+    seg.push_back(pg);
+  }
+  qc_status r = flush();
+  if (r != QC_OK) return r;
+  P->layout_out.assign(lay, lay + n);
+  return QC_OK;
+}
+
+qc_status enqueue_dist(qc_state* s, DistPlan* P) {
+  const uint64_t nloc_amps = 1ull << s->n_loc;
+  for (auto& st : P->steps) {
+    if (st.kind == 1) {
+      const qc_status r = dist_exchange(s, st.g, st.l);
+      if (r != QC_OK) return r;
+      continue;
+    }
+    if (s->dist == 1) {
+      for (int v = 0; v < s->world; ++v) {
+        const uint64_t rb = (uint64_t)v * nloc_amps;
+        const int e = enqueue_entry(s, st.seg.get(), s->stream, s->d, rb, rb);
+        if (e) return cuda_fail(s, e, "fused pass (loopback shard)");
+      }
+    } else {
+      const uint64_t rb = (uint64_t)s->rank * nloc_amps;
+      const int e = enqueue_entry(s, st.seg.get(), s->stream, s->d, rb, 0);
+      if (e) return cuda_fail(s, e, "fused pass (shard)");
+    }
+  }
+  return QC_OK;
+}
+
+}  // namespace
+
+// Host-only schedule for tests (qc_debug.h): steps as (kind, g, l, gates).
+qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
+                            std::vector<int>& out, std::vector<int>& layout_out) {
+  qc_state s;
+  s.n = n;
+  s.world = world;
+  s.n_loc = n - std::countr_zero((unsigned)world);
+  s.relabel = relabel;
+  s.dist = 1;
+  for (int q = 0; q < n; ++q) s.layout[q] = n - 1 - q;
+  DistPlan P;
+  const qc_status r = build_dist_plan(&s, ops, n_ops, &P, true);
+  if (r != QC_OK) return r;
+  for (auto& st : P.steps) {
+    out.push_back(st.kind);
+    out.push_back(st.g);
+    out.push_back(st.l);
+    out.push_back(st.kind == 0 ? (int)st.seg->fused_gates : 0);
+  }
+  layout_out = P.layout_out;
+  return QC_OK;
+}
+
+qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  {
+    const qc_status c = ensure_fused_configured(s);
+    if (c != QC_OK) return c;
+  }
+  const uint64_t salt = 0xd157ull ^ ((uint64_t)s->relabel << 2) ^ ((uint64_t)s->block_fusion << 3) ^
+                        ((uint64_t)s->tile_bits << 8) ^ ((uint64_t)s->row_bits << 16) ^
+                        ((uint64_t)s->tma_mode << 24) ^ ((uint64_t)s->jit << 28);
+  const uint64_t key = hash_ops(ops, n_ops, s->layout, s->n, salt);
+  DistPlan* P = nullptr;
+  if (!s->dcache) s->dcache = new DistCache();
+  auto& dplans = s->dcache->plans;
+  auto it = dplans.find(key);
+  if (it != dplans.end() && it->second->ops.size() == n_ops &&
+      std::memcmp(it->second->ops.data(), ops, n_ops * sizeof(qc_gate)) == 0 &&
+      std::memcmp(it->second->layout_in.data(), s->layout, sizeof(int) * s->n) == 0) {
+    P = it->second.get();
+  } else {
+    auto np = std::make_unique<DistPlan>();
+    np->ops.assign(ops, ops + n_ops);
+    np->layout_in.assign(s->layout, s->layout + s->n);
+    const qc_status r = build_dist_plan(s, ops, n_ops, np.get());
+    if (r != QC_OK) return r;
+    P = np.get();
+    if (dplans.size() > 32) dplans.clear();
+    dplans[key] = std::move(np);
+  }
+  P->uses++;
+  for (auto& st : P->steps) {
+    if (st.kind != 0) continue;
+    st.seg->uses = P->uses;
+    const qc_status r = maybe_jit(s, st.seg.get());
+    if (r != QC_OK) return r;
+  }
+  const qc_status r = enqueue_dist(s, P);
+  if (r != QC_OK) return r;
+  std::memcpy(s->layout, P->layout_out.data(), sizeof(int) * s->n);
+  int64_t launches = 0;
+  bool jit = true;
+  for (auto& st : P->steps)
+    if (st.kind == 0) {
+      launches += (int64_t)st.seg->passes.size() * (s->dist == 1 ? s->world : 1);
+      jit = jit && st.seg->jit_state == 1;
+    }
+  s->last_passes = P->passes;
+  s->last_launches = launches;
+  s->last_relabels = P->relabels;
+  s->last_exchanges = P->exchanges;
+  s->last_graph = 0;
+  s->last_jit = jit ? 1 : 0;
+  return QC_OK;
+}
+
+// Restore the canonical layout (collective): local pairs by SWAP2 kernels on
+// each shard, pairs involving rank bits by exchanges through local bit n_loc-1.
+qc_status dist_canonicalize(qc_state* s) {
+  const int n = s->n, nl = s->n_loc, L = nl - 1;
+  auto phys_swap = [&](int a, int b) -> qc_status {  // swap physical bits a, b (a != b)
+    if (a < nl && b < nl) {
+      PGate g;
+      g.kind = GK::SWAP2;
+      g.t0 = a;
+      g.t1 = b;
+      if (s->dist == 1) {
+        // loopback: the buffer is the whole state, a local bit swap is a swap on n bits
+        const int e = launch_gate(s->d, n, s->dbl, g, s->stream);
+        if (e) return cuda_fail(s, e, "canonicalize swap");
+      } else {
+        const int e = launch_gate(s->d, nl, s->dbl, g, s->stream);
+        if (e) return cuda_fail(s, e, "canonicalize swap");
+      }
+      return QC_OK;
+    }
+    if (a >= nl && b >= nl) {  // two rank bits: through the slot
+      qc_status r = dist_exchange(s, a, L);
+      if (r == QC_OK) r = dist_exchange(s, b, L);
+      if (r == QC_OK) r = dist_exchange(s, a, L);
+      return r;
+    }
+    const int g = a >= nl ? a : b, l = a >= nl ? b : a;
+    if (l == L) return dist_exchange(s, g, L);
+    // g <-> l == (l<->L) (g<->L) (l<->L)
+    qc_status r = QC_OK;
+    PGate sw;
+    sw.kind = GK::SWAP2;
+    sw.t0 = L;
+    sw.t1 = l;
+    auto local_sw = [&]() -> qc_status {
+      const int e = launch_gate(s->d, s->dist == 1 ? n : nl, s->dbl, sw, s->stream);
+      return e ? cuda_fail(s, e, "canonicalize swap") : QC_OK;
+    };
+    r = local_sw();
+    if (r == QC_OK) r = dist_exchange(s, g, L);
+    if (r == QC_OK) r = local_sw();
+    return r;
+  };
+  for (int q = 0; q < n; ++q) {
+    const int want = n - 1 - q;
+    if (s->layout[q] == want) continue;
+    int q2 = -1;
+    for (int u = 0; u < n; ++u)
+      if (s->layout[u] == want) q2 = u;
+    const qc_status r = phys_swap(s->layout[q], want);
+    if (r != QC_OK) return r;
+    s->layout[q2] = s->layout[q];
+    s->layout[q] = want;
+  }
+  return QC_OK;
+}
+
+}  // namespace qc

@@ -269,7 +269,7 @@ void setup_bits(Block& B, uint64_t bits) {
 
 }  // namespace
 
-std::vector<PGate> fuse_blocks(const std::vector<PGate>& in) {
+std::vector<PGate> fuse_blocks(const std::vector<PGate>& in, uint64_t local_mask) {
   std::vector<Block> blocks;
   blocks.reserve(in.size());
   int last[64];
@@ -280,7 +280,7 @@ std::vector<PGate> fuse_blocks(const std::vector<PGate>& in) {
     // candidate blocks: the latest item on each of g's bits
     int cand[3];
     int nc = 0;
-    bool ok = std::popcount(Q) <= 2;
+    bool ok = std::popcount(Q) <= 2 && !(Q & ~local_mask);
     for (int p = 0; p < 64 && ok; ++p) {
       if (!(Q & (1ull << p)) || last[p] < 0) continue;
       const int bi = last[p];
@@ -298,7 +298,7 @@ std::vector<PGate> fuse_blocks(const std::vector<PGate>& in) {
     if (ok && std::popcount(U) > 2) ok = false;
 
     Block NB;
-    if (std::popcount(Q) > 2) {
+    if (std::popcount(Q) > 2 || (Q & ~local_mask)) {  // > 2 bits, or touches a rank bit: keep as is
       NB.raw = true;
       NB.bits = Q;
       NB.g = g;

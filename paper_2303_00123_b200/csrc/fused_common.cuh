@@ -369,7 +369,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
       if (i >= NBUF) {  // buffer b holds finished tile i-NBUF: write it back
         const uint64_t ip = i - NBUF;
         qc_mbar_wait(&empty[b], (uint32_t)((ip / NBUF) & 1ull));
-        const uint64_t base = qc_tile_base(pd, blockIdx.x + ip * gridDim.x);
+        const uint64_t base = qc_tile_base(pd, blockIdx.x + ip * gridDim.x) | pd.addr_bits;
         if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)
             qc_scatter4(tmap, (int32_t)((base | row_off[r]) >> rb), (int32_t)((base | row_off[r + 1]) >> rb),
@@ -384,7 +384,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
         __syncwarp();
       }
       if (i < my_n) {
-        const uint64_t base = qc_tile_base(pd, blockIdx.x + i * gridDim.x);
+        const uint64_t base = qc_tile_base(pd, blockIdx.x + i * gridDim.x) | pd.addr_bits;
         if (lane == 0) {
           buf_tile[b] = (uint32_t)i;  // full[b]'s pending phase now belongs to tile i
           qc_mbar_arrive_expect_tx(&full[b], tile_bytes);
@@ -411,7 +411,9 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   for (uint64_t i = (uint64_t)(tid / kGroupThreads); i < my_n; i += kGroups) {
     const int b = (int)(i % NBUF);
     const int par = (int)(i % kWSlots);
-    const uint64_t tbase = qc_tile_base(pd, blockIdx.x + i * gridDim.x);
+    // global index of the tile's first amplitude (rank bits included): used
+    // for control predicates and diagonal bits; memory addresses stay local
+    const uint64_t tbase = qc_tile_base(pd, blockIdx.x + i * gridDim.x) | pd.rank_bits;
     body.prologue(tbase, par);
     if (kGroups > 1 && NBUF % kGroups) {
       // wait until the producer has claimed buffer b for this tile (see fused_types.h)

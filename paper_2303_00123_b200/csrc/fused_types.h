@@ -83,6 +83,10 @@ struct PassDesc {
   uint32_t blob_bytes;    // [subs][hdrs][coefs][terms], 16-byte aligned sections
   uint32_t n_sub, n_ops, n_prun;
   uint32_t off_hdr, off_coef, off_term;  // section offsets inside the pass blob
+  uint32_t pad_;
+  uint64_t rank_bits;     // sharded state: this rank's global bits (rank << n_loc), OR-ed
+                          // into every tile's base for predicates / diagonal bits only
+  uint64_t addr_bits;     // OR-ed into amplitude addresses (loopback: shards share one buffer)
 };
 
 }  // namespace qc

@@ -26,28 +26,43 @@ __device__ __forceinline__ double u_pm1(uint64_t x) {
   return __dsub_rn(__dmul_rn((double)(x >> 11), 0x1p-52), 1.0);
 }
 
+// Amplitude j of the buffer is global amplitude first + j.
 template <typename C>
-__global__ void init_random_kernel(C* s, uint64_t N, uint64_t seed, double scale);
+__global__ void init_random_kernel(C* s, uint64_t N, uint64_t first, uint64_t seed, double scale);
 
 template <>
-__global__ void init_random_kernel<double2>(double2* s, uint64_t N, uint64_t seed, double scale) {
+__global__ void init_random_kernel<double2>(double2* s, uint64_t N, uint64_t first, uint64_t seed,
+                                            double scale) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += stride) {
+    const uint64_t i = first + j;
     double2 v;
     v.x = __dmul_rn(u_pm1(splitmix64(seed, 2 * i)), scale);
     v.y = __dmul_rn(u_pm1(splitmix64(seed, 2 * i + 1)), scale);
-    s[i] = v;
+    s[j] = v;
   }
 }
 
 template <>
-__global__ void init_random_kernel<float2>(float2* s, uint64_t N, uint64_t seed, double scale) {
+__global__ void init_random_kernel<float2>(float2* s, uint64_t N, uint64_t first, uint64_t seed,
+                                           double scale) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += stride) {
+    const uint64_t i = first + j;
     float2 v;
     v.x = __double2float_rn(__dmul_rn(u_pm1(splitmix64(seed, 2 * i)), scale));
     v.y = __double2float_rn(__dmul_rn(u_pm1(splitmix64(seed, 2 * i + 1)), scale));
-    s[i] = v;
+    s[j] = v;
+  }
+}
+
+// Swap two equal, disjoint device ranges (loopback exchange), 16-byte units.
+__global__ void swap_regions_kernel(uint4* __restrict__ a, uint4* __restrict__ b, uint64_t n16) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n16; j += stride) {
+    const uint4 x = a[j], y = b[j];
+    a[j] = y;
+    b[j] = x;
   }
 }
 
@@ -107,14 +122,22 @@ unsigned blocks_for(uint64_t count, int threads) {
 
 }  // namespace
 
-int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream) {
+int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream, uint64_t first,
+                       uint64_t count) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const uint64_t N = 1ull << n;
-  const double scale = std::sqrt(1.5 / (double)N);
+  const uint64_t N = count ? count : (1ull << n);
+  const double scale = std::sqrt(1.5 / (double)(1ull << n));  // normalisation of the global state
   if (dbl)
-    init_random_kernel<double2><<<blocks_for(N, 256), 256, 0, st>>>((double2*)state, N, seed, scale);
+    init_random_kernel<double2><<<blocks_for(N, 256), 256, 0, st>>>((double2*)state, N, first, seed, scale);
   else
-    init_random_kernel<float2><<<blocks_for(N, 256), 256, 0, st>>>((float2*)state, N, seed, scale);
+    init_random_kernel<float2><<<blocks_for(N, 256), 256, 0, st>>>((float2*)state, N, first, seed, scale);
+  return (int)cudaGetLastError();
+}
+
+int launch_swap_regions(void* a, void* b, uint64_t bytes, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t n16 = bytes / 16;
+  swap_regions_kernel<<<blocks_for(n16, 256), 256, 0, st>>>((uint4*)a, (uint4*)b, n16);
   return (int)cudaGetLastError();
 }
 

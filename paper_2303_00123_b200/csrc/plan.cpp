@@ -328,6 +328,8 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates) {
     d.rb = rb;
     d.pshift = rb;
     d.g4 = 0;
+    d.rank_bits = 0;
+    d.addr_bits = 0;
     d.n_hi = 0;
     for (int p = rb; p < n; ++p)
       if (T & (1ull << p)) d.hi_pos[d.n_hi++] = p;

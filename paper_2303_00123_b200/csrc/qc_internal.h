@@ -52,7 +52,9 @@ uint64_t pgate_bits(const PGate& g);            // targets | controls
 void pgate_dense4(const PGate& g, cd out[16]);  // 2-bit kinds as a dense 4x4
 
 // Host block fusion (fuse.cpp): merge gates on <= 2 bits, classify exactly.
-std::vector<PGate> fuse_blocks(const std::vector<PGate>& in);
+// local_mask: bits a merged block may act on (rank bits of a sharded state
+// stay out of blocks; gates touching them pass through unchanged).
+std::vector<PGate> fuse_blocks(const std::vector<PGate>& in, uint64_t local_mask);
 
 // ------------------------------------------------------- fused encoding
 // FHdr, FTermT, SubStageDesc, PassDesc, op kinds / patterns: fused_types.h
@@ -114,7 +116,9 @@ int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_b
                       int ctas, void* stream);
 bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out);
 int fused_configure(bool dbl);
-int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream);
+int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream, uint64_t first = 0,
+                       uint64_t count = 0);
+int launch_swap_regions(void* a, void* b, uint64_t bytes, void* stream);
 int launch_init_basis(void* state, int n, bool dbl, uint64_t k, void* stream);
 // gather canonical [first, first+count) from a permuted layout into dst (device)
 int launch_gather(const void* state, void* dst, int n, bool dbl, const int* layout,

@@ -1,0 +1,116 @@
+// state.h -- internal definition of qc_state and the cached plans (shared by
+// api.cu and dist.cu).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "qc_internal.h"
+
+namespace qc {
+
+struct PlanEntry {
+  std::vector<qc_gate> ops;          // exact copy (collision check)
+  std::vector<int> layout_in, layout_out;
+  std::vector<PassDesc> passes;
+  void* d_blob = nullptr;
+  int64_t fused_gates = 0;
+  std::shared_ptr<FusedPlan> ir;     // kept for JIT specialisation
+  std::vector<JitKernel> jit;
+  int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
+  QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
+  bool dbl = true;
+  int64_t relabels = 0;
+  int uses = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int ctas = 0;
+  int tile_bits = 0;
+  ~PlanEntry() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (d_blob) cudaFree(d_blob);
+  }
+};
+
+
+struct DistPlan;   // dist.cu
+struct DistCache;  // dist.cu
+
+// api.cu helpers shared with dist.cu
+qc_status fail(qc_status st, const char* fmt, ...);
+qc_status cuda_fail(qc_state* s, int e, const char* what);
+PGate lower(const qc_gate& g, const int* layout);
+qc_status validate_gate(int n, const qc_gate& g, size_t idx);
+uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt);
+qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
+                            PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0);
+int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
+                  uint64_t addr_bits);
+qc_status maybe_jit(qc_state* s, PlanEntry* e);
+qc_status ensure_fused_configured(qc_state* s);
+extern const int kArity[16];
+extern const int kNctrl[16];
+
+// dist.cu
+qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops);
+qc_status dist_canonicalize(qc_state* s);
+qc_status dist_exchange(qc_state* s, int g, int l);
+qc_status nccl_create_comm(qc_state* s, const void* unique_id);
+qc_status nccl_get_unique_id(void* out128);
+qc_status nccl_allreduce_sum(qc_state* s, double* host_value);
+void nccl_destroy(qc_state* s);
+void dist_release(qc_state* s);  // drop sharded plans + communicator
+qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
+                            std::vector<int>& out, std::vector<int>& layout_out);
+struct ExchangeRun {
+  uint64_t offset;  // amplitudes, within the shard
+  uint64_t count;
+};
+// The part of rank `rank`'s shard that an exchange of global bit g with local
+// bit l sends (and receives into): local indices y with bit l == 1 - bit g.
+std::vector<ExchangeRun> exchange_runs(int n_loc, int rank, int g, int l, int* partner);
+
+}  // namespace qc
+
+struct qc_state {
+  int n = 0;
+  qc_precision prec = QC_COMPLEX128;
+  bool dbl = true;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* d = nullptr;
+  bool own_mem = false;
+  size_t bytes = 0;
+  int layout[64];
+  bool failed = false;
+  // options
+  int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0, block_fusion = 1, jit = 1;
+  int row_bits = 0, tma_mode = 0;
+  std::string jit_error;
+  // stats
+  int64_t last_gates = 0, last_passes = 0, last_launches = 0, last_relabels = 0;
+  int last_graph = 0, last_k = 0;
+  int64_t last_blocks = 0;
+  int last_jit = 0;
+  // plan cache
+  std::unordered_map<uint64_t, std::unique_ptr<qc::PlanEntry>> plans;
+  cudaStream_t cap_stream = nullptr;
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  double* d_partial = nullptr;
+  // sharded state: physical bits >= n_loc are rank bits
+  int dist = 0;       // 0: single GPU; 1: loopback (all ranks' shards in this buffer); 2: NCCL
+  int world = 1, rank = 0, n_loc = 0;
+  void* nccl_comm = nullptr;
+  void* d_xstage = nullptr;
+  size_t xstage_bytes = 0;
+  int64_t last_exchanges = 0;
+  qc::DistCache* dcache = nullptr;  // sharded plans (owned by dist.cu)
+  ~qc_state();
+};
+

@@ -36,6 +36,7 @@ GATE_DTYPE = np.dtype([("op", "<i4"), ("qubits", "<i4", (3,)), ("ctrl_state", "<
 assert GATE_DTYPE.itemsize == 288
 
 EXPORTS = ["qc_state_create", "qc_state_create_ex", "qc_state_wrap", "qc_state_destroy",
+           "qc_state_create_dist", "qc_state_create_loopback", "qc_nccl_unique_id",
            "qc_state_init_basis", "qc_state_init_random", "qc_apply_gate", "qc_run_circuit",
            "qc_state_read", "qc_state_write", "qc_state_canonicalize", "qc_state_sync",
            "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_last_error", "qc_version"]
@@ -55,7 +56,8 @@ class qc_info(ctypes.Structure):
                 ("last_launches", ctypes.c_int64), ("last_relabels", ctypes.c_int64),
                 ("last_graph", ctypes.c_int32), ("tile_bits", ctypes.c_int32),
                 ("last_blocks", ctypes.c_int64), ("last_jit", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("n_local", ctypes.c_int32),
+                ("sharding", ctypes.c_int32), ("last_exchanges", ctypes.c_int64)]
 
 
 class qc_plan_stats(ctypes.Structure):
@@ -66,7 +68,7 @@ class qc_plan_stats(ctypes.Structure):
                 ("jit_compiled", ctypes.c_int32)]
 
 
-DEBUG_EXPORTS = ["qc_debug_plan"]
+DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule"]
 
 _lib = None
 
@@ -100,6 +102,14 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
                                 ctypes.c_char_p, sz]
     L.qc_debug_plan.restype = ctypes.c_int
+    L.qc_state_create_dist.argtypes = [i32, i32, i32, i32, vp, ctypes.POINTER(vp)]
+    L.qc_state_create_loopback.argtypes = [i32, i32, i32, ctypes.POINTER(vp)]
+    L.qc_nccl_unique_id.argtypes = [vp]
+    L.qc_debug_exchange_runs.argtypes = [i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int), vp, vp, i32,
+                                         ctypes.POINTER(ctypes.c_int)]
+    L.qc_debug_exchange_runs.restype = ctypes.c_int
+    L.qc_debug_dist_schedule.argtypes = [i32, i32, i32, vp, sz, vp, i32, ctypes.POINTER(ctypes.c_int), vp]
+    L.qc_debug_dist_schedule.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
     L.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -153,6 +163,21 @@ class State:
         h = ctypes.c_void_p()
         _check(lib().qc_state_create_ex(n, PRECISION[precision], device, stream, ctypes.byref(h)))
         self._h = h
+
+    @classmethod
+    def loopback(cls, n: int, precision: str, world: int) -> "State":
+        """All `world` shards of a sharded state in this process / GPU (validation)."""
+        h = ctypes.c_void_p()
+        _check(lib().qc_state_create_loopback(n, PRECISION[precision], world, ctypes.byref(h)))
+        return cls(n, precision, _handle=h)
+
+    @classmethod
+    def dist(cls, n: int, precision: str, rank: int, world: int, nccl_id: bytes) -> "State":
+        """This rank's shard (one process per GPU, NCCL); collective."""
+        h = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().qc_state_create_dist(n, PRECISION[precision], rank, world, idbuf, ctypes.byref(h)))
+        return cls(n, precision, _handle=h)
 
     @classmethod
     def wrap(cls, n: int, precision: str, dev_ptr: int, stream: Optional[int] = None) -> "State":
@@ -245,7 +270,9 @@ class State:
                 "last_gates": i.last_gates, "last_passes": i.last_passes,
                 "last_launches": i.last_launches, "last_relabels": i.last_relabels,
                 "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits,
-                "last_blocks": i.last_blocks, "last_jit": bool(i.last_jit)}
+                "last_blocks": i.last_blocks, "last_jit": bool(i.last_jit), "world": i.world,
+                "rank": i.rank, "n_local": i.n_local, "sharding": i.sharding,
+                "last_exchanges": i.last_exchanges}
 
     @property
     def stream(self) -> int:
@@ -266,6 +293,37 @@ def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_f
     if rc != QC_OK:
         raise QCError(rc, eb.value.decode())
     return {f: getattr(st, f) for f, _ in qc_plan_stats._fields_}
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().qc_nccl_unique_id(buf))
+    return buf.raw
+
+
+def debug_exchange_runs(n_loc: int, rank: int, g: int, l: int):
+    """(partner, [(offset, count), ...]) of a qubit-swap exchange (host only)."""
+    partner, nr = ctypes.c_int(), ctypes.c_int()
+    cap = 1 << 16
+    offs = np.zeros(cap, dtype=np.uint64)
+    cnts = np.zeros(cap, dtype=np.uint64)
+    _check(lib().qc_debug_exchange_runs(n_loc, rank, g, l, ctypes.byref(partner), offs.ctypes.data,
+                                        cnts.ctypes.data, cap, ctypes.byref(nr)))
+    return partner.value, [(int(offs[i]), int(cnts[i])) for i in range(min(nr.value, cap))]
+
+
+def debug_dist_schedule(n: int, world: int, ops, relabel: bool = True):
+    """Host-only sharded schedule: ([(kind, g, l, gates)], final layout)."""
+    arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
+    arr = np.ascontiguousarray(arr)
+    cap = 1 << 14
+    steps = np.zeros(4 * cap, dtype=np.int32)
+    lay = np.zeros(64, dtype=np.int32)
+    ns = ctypes.c_int()
+    _check(lib().qc_debug_dist_schedule(n, world, int(relabel), arr.ctypes.data if len(arr) else None,
+                                        len(arr), steps.ctypes.data, cap, ctypes.byref(ns), lay.ctypes.data))
+    out = [tuple(int(x) for x in steps[4 * i:4 * i + 4]) for i in range(min(ns.value, cap))]
+    return out, [int(x) for x in lay[:n]]
 
 
 def version() -> str:

@@ -42,7 +42,7 @@ def test_gate_struct_layout_matches_header():
     assert qc.GATE_DTYPE.itemsize == 288
     assert qc.GATE_DTYPE.fields["theta"][1] == 24
     assert qc.GATE_DTYPE.fields["m"][1] == 32
-    assert ctypes.sizeof(qc.qc_info) == 4 + 4 + 8 + 8 + 256 + 4 + 4 + 8 * 4 + 4 + 4 + 8 + 4 + 4
+    assert ctypes.sizeof(qc.qc_info) == 368  # natural alignment of the qc_info fields in qc.h
 
 
 def test_op_codes_match_header():
