@@ -37,12 +37,16 @@ CONFIGS = {
     "qft30": ("qft", 30, 0, "c128", "QFT on 30 qubits, complex double, 1 B200"),
     "qft30c64": ("qft", 30, 0, "c64", "QFT on 30 qubits, complex single, 1 B200"),
     "tfxy33": ("tfxy", 33, 10, "c128", "TFXY Trotter circuit, 33 qubits complex double, 1 B200"),
+    # sharded (one process per GPU, NCCL qubit-swap exchanges): n = local + log2(N)
+    "qft_shard": ("qft", None, 0, "c128",
+                  "QFT complex double sharded over N B200 by the top log2(N) qubits (weak scaling)"),
 }
 
 
-def build_ops(cfg):
+def build_ops(cfg, n=None):
     import qcgen
-    fam, n, steps, prec, _ = CONFIGS[cfg]
+    fam, n0, steps, prec, _ = CONFIGS[cfg]
+    n = n0 if n is None else n
     return qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, steps)
 
 
@@ -107,13 +111,14 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU oracle
-def cpu_oracle_rate(cfg: str, budget_s: float = 15.0):
+def cpu_oracle_rate(cfg: str, budget_s: float = 15.0, n_override=None):
     """Time the oracle (as it stands) on the host cores on a bounded prefix of
     the same circuit; returns circuits/s extrapolated from the prefix."""
     import oracle
     import qcgen
     fam, n, steps, prec, _ = CONFIGS[cfg]
-    ops = build_ops(cfg)
+    n = n if n_override is None else n_override
+    ops = build_ops(cfg, n)
     n_s = min(n, 24)  # largest size the host holds comfortably for a bounded sample
     st = qcgen.random_state(n_s, precision=prec)
     sample_ops = ops if n_s == n else [o for o in ops if max(o.qubits) < n_s]
@@ -257,6 +262,92 @@ def _time_runs(s, arr, warm=4, reps=3):
     return a.elapsed_time(b) / reps
 
 
+def run_sharded(args, rank, world, local_rank):
+    """QFT on a state sharded over `world` GPUs (qc_state_create_dist, NCCL
+    send/recv exchanges); weak scaling: 2^local_qubits amplitudes per GPU."""
+    import torch
+    import paper_2303_00123_b200 as qc
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = world.bit_length() - 1
+    n = args.local_qubits + p
+    prec = "c128"
+    ops = build_ops(args.config, n)
+    arr = qc.encode_ops(ops)
+    if world > 1:
+        uid = [qc.qc.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        s = qc.State.dist(n, prec, rank, world, uid[0])
+    else:
+        s = qc.State(n, prec, device=local_rank)
+    stream = torch.cuda.ExternalStream(s.stream, device=dev)
+    s.init_random(12345)
+    ab = 16
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            s.run(arr)
+        torch.cuda.synchronize()
+        info = s.info()
+        if world > 1:
+            torch.distributed.barrier()
+        clk = ClockSampler(local_rank)
+        clk.start()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            s.run(arr)
+        b.record(stream)
+        torch.cuda.synchronize()
+        clocks = clk.stop()
+        t = a.elapsed_time(b)
+        ex = None
+        if world > 1:  # NVLink: one exchange of the top rank bit with the top local bit, timed alone
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 4
+            e0.record(stream)
+            for _ in range(reps):
+                s.exchange(n - 1, n - p - 1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            te = e0.elapsed_time(e1) / reps
+            bytes_dir = (ab << (n - p)) // 2
+            ex = {"ms": te, "bytes_per_direction": bytes_dir, "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9}
+    tt = torch.tensor([t], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        if ex is not None:
+            te_t = torch.tensor([ex["ms"]], device=dev)
+            torch.distributed.all_reduce(te_t, op=torch.distributed.ReduceOp.MAX)
+            ex["ms"] = float(te_t.item())
+            ex["GBps_per_direction"] = ex["bytes_per_direction"] / (ex["ms"] / 1e3) / 1e9
+    t = float(tt.item())
+    ms = t / args.steps
+    peak, kind = load_peaks()
+    sb_loc = ab << (n - p)
+    out = {
+        "metric": METRIC, "value": 1e3 / ms, "unit": "circuit/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][4], "circuit": "qft", "qubits": n,
+                   "local_qubits": n - p, "precision": prec, "parallelism": f"sharded x{world} (NCCL)",
+                   "exchanges_per_step": info.get("last_exchanges", 0),
+                   "fused_passes_per_step": info["last_passes"], "jit_specialised": info["last_jit"],
+                   "l2": f"state {sb_loc >> 20} MiB per GPU >> 126 MB L2"},
+        "gpu_launches": int(info["last_launches"] * args.steps),
+        "roofline": {"bound": "hbm", "kernel": "qc_pass (fused tile pass, per shard)",
+                     "achieved": 2 * sb_loc * info["last_passes"] / (ms / 1e3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "traffic": None,
+                     "note": "lower bound: step time includes exchanges"},
+        "nvlink_exchange": ex, "clocks": clocks,
+    }
+    out["roofline"]["frac"] = out["roofline"]["achieved"] / peak
+    if ex is not None:
+        out["nvlink_exchange"]["frac_of_900"] = ex["GBps_per_direction"] / 900.0
+    s.close()
+    return out
+
+
 def sweep(args, local_rank):
     """Single-GPU measurements beside the main line (BASELINE metric: circuit
     time vs qubits; per-gate HBM GB/s vs peak; fused-pass GB/s)."""
@@ -317,7 +408,9 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     fam, n, steps_c, prec, desc = CONFIGS[args.config]
-    rate, cores, sample = cpu_oracle_rate(args.config, budget_s=max(5.0, 4.0 * args.steps))
+    if n is None:  # sharded config: the whole state, n = local + log2(N)
+        n = args.local_qubits + (world.bit_length() - 1)
+    rate, cores, sample = cpu_oracle_rate(args.config, budget_s=max(5.0, 4.0 * args.steps), n_override=n)
     return {"impl": "reference", "metric": METRIC, "value": rate, "unit": "circuit/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "weak",
@@ -338,6 +431,7 @@ def main():
     ap.add_argument("--config", default="tfxy20", choices=sorted(CONFIGS))
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--local-qubits", type=int, default=30, help="qft_shard: qubits per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 5)  # JIT on 2nd use + graph capture; QFT relabels alternate plans
     rank = int(os.environ.get("RANK", 0))
@@ -354,6 +448,14 @@ def main():
     if world > 1:
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.config == "qft_shard":
+        out = run_sharded(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
     out = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1:
         if not args.no_sweep:

@@ -48,6 +48,11 @@ qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, int* partner
 qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
                                  int* steps, int max_steps, int* n_steps, int* layout_out);
 
+/* Run one qubit-swap exchange of physical rank bit g with local bit l on a
+ * sharded state (collective; enqueued on the state's stream); the layout is
+ * updated.  Used to time NVLink exchanges in isolation. */
+qc_status qc_debug_exchange(qc_state* s, int g, int l);
+
 #ifdef __cplusplus
 }
 #endif

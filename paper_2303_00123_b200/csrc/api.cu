@@ -849,3 +849,18 @@ extern "C" qc_status qc_debug_dist_schedule(int n, int world, int relabel, const
   if (layout_out) std::memcpy(layout_out, lay.data(), sizeof(int) * lay.size());
   return QC_OK;
 }
+
+extern "C" qc_status qc_debug_exchange(qc_state* s, int g, int l) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if (!s->dist) return fail(QC_ERR_INVALID_ARG, "state is not sharded");
+  if (g < s->n_loc || g >= s->n || l < 0 || l >= s->n_loc) return fail(QC_ERR_INVALID_ARG, "bad bits");
+  st = dist_exchange(s, g, l);
+  if (st != QC_OK) return st;
+  // the data now has physical bits g and l swapped: keep the layout truthful
+  for (int q = 0; q < s->n; ++q) {
+    if (s->layout[q] == g) s->layout[q] = l;
+    else if (s->layout[q] == l) s->layout[q] = g;
+  }
+  return QC_OK;
+}

@@ -68,7 +68,7 @@ class qc_plan_stats(ctypes.Structure):
                 ("jit_compiled", ctypes.c_int32)]
 
 
-DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule"]
+DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange"]
 
 _lib = None
 
@@ -110,6 +110,8 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_exchange_runs.restype = ctypes.c_int
     L.qc_debug_dist_schedule.argtypes = [i32, i32, i32, vp, sz, vp, i32, ctypes.POINTER(ctypes.c_int), vp]
     L.qc_debug_dist_schedule.restype = ctypes.c_int
+    L.qc_debug_exchange.argtypes = [vp, i32, i32]
+    L.qc_debug_exchange.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
     L.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -247,6 +249,10 @@ class State:
 
     def read_ptr(self, host_ptr: int, count: int, first: int = 0):
         _check(lib().qc_state_read(self._h, first, count, host_ptr))
+
+    def exchange(self, g: int, l: int):
+        """One qubit-swap exchange of physical rank bit g with local bit l (debug)."""
+        _check(lib().qc_debug_exchange(self._h, g, l))
 
     def canonicalize(self):
         _check(lib().qc_state_canonicalize(self._h))

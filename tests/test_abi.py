@@ -13,8 +13,8 @@ from paper_2303_00123_b200 import qc
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    txt = open(os.path.join(ROOT, "include", "qc.h")).read()
+def declared_symbols(header="qc.h"):
+    txt = open(os.path.join(ROOT, "include", header)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(qc_[a-z0-9_]+)\s*\(", txt)))
 
@@ -30,6 +30,9 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(L, s)]
     assert not missing, missing
     assert sorted(qc.EXPORTS) == declared_symbols()
+    dbg = declared_symbols("qc_debug.h")
+    assert not [x for x in dbg if not hasattr(L, x)]
+    assert sorted(qc.DEBUG_EXPORTS) == dbg
 
 
 def test_version_string():
