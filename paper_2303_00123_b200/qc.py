@@ -16,7 +16,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqc.so")
+LIB_PATH = os.environ.get("QC_LIB", os.path.join(_HERE, "libqc.so"))
 
 QC_OK, QC_ERR_INVALID_ARG, QC_ERR_OUT_OF_MEMORY, QC_ERR_CUDA, QC_ERR_NCCL, \
     QC_ERR_UNSUPPORTED, QC_ERR_STATE_FAILED = range(7)
