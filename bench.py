@@ -378,6 +378,22 @@ def sweep(args, local_rank):
             res["circuit_ms_vs_qubits"][key][str(n)] = entry
             s.close()
             torch.cuda.empty_cache()
+    # north-star capacity: configs C4 (TFXY n=33, 10 steps) and QFT n=33, complex128, 137 GB
+    res["north_star_n33_c128"] = {}
+    free, _ = torch.cuda.mem_get_info()
+    if free > (16 << 33) * 1.05:
+        for fam in ("tfxy", "qft"):
+            ops = qcgen.qft(33) if fam == "qft" else qcgen.tfxy(33, 10)
+            s = qc.State(33, "c128", device=local_rank)
+            s.init_random(1)
+            t = _time_runs(s, qc.encode_ops(ops), warm=4 if fam == "qft" else 2, reps=2)
+            inf = s.info()
+            gbps = 2 * (16 << 33) * inf["last_passes"] / (t / 1e3) / 1e9
+            res["north_star_n33_c128"][f"{fam}33" + ("_S10" if fam == "tfxy" else "")] = {
+                "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
+                "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
+            s.close()
+            torch.cuda.empty_cache()
     for prec in ("c128", "c64"):
         n = 30
         sb = (16 if prec == "c128" else 8) << n

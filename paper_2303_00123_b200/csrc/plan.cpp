@@ -16,6 +16,7 @@
 // order, so the product of the passes is the circuit (eq:kron in order).
 #include <algorithm>
 #include <bit>
+#include <cmath>
 #include <cstring>
 
 #include "qc_internal.h"
@@ -182,6 +183,46 @@ FOpIR convert(const PGate& g, const Ctx& c) {
   rows_to_ir(M, 2, o);
   for (int i = 0; i < 4; ++i) o.dense[i] = M[i];
   return o;
+}
+
+// Within one pass every amplitude of a tile sees every unpredicated op once,
+// and scalars commute with everything: pull a common real magnitude c out of
+// each unpredicated M op (the Hadamards' 1/sqrt2, making H blocks +-1
+// additions) and fold the product into the pass's first unpredicated M op.
+void factor_pass_scalars(FusedPassPlan& pp) {
+  FOpIR* first = nullptr;
+  double C = 1.0;
+  for (auto& o : pp.ops) {
+    if (o.h.kind != F_M1 && o.h.kind != F_M2) continue;
+    if (o.h.smask || o.h.lmask || o.h.omask) continue;
+    if (o.h.dsrc == P_MOVE) continue;  // permutations stay pure moves
+    const int dim = o.h.kind == F_M1 ? 2 : 4;
+    if (!first) {
+      first = &o;
+      continue;
+    }
+    double c = 0;
+    bool ok = true;
+    for (int i = 0; i < dim * dim && ok; ++i) {
+      const double m = std::abs(o.dense[i]);
+      if (m == 0) continue;
+      if (c == 0) c = m;
+      else if (std::fabs(m - c) > 1e-14 * c) ok = false;
+    }
+    if (!ok || c == 0 || c == 1.0) continue;
+    for (int i = 0; i < dim * dim; ++i) o.dense[i] /= c;
+    C *= c;
+    o.coefs.clear();
+    o.h.identmask = 0;
+    rows_to_ir(o.dense, dim, o);
+  }
+  if (first && C != 1.0) {
+    const int dim = first->h.kind == F_M1 ? 2 : 4;
+    for (int i = 0; i < dim * dim; ++i) first->dense[i] *= C;
+    first->coefs.clear();
+    first->h.identmask = 0;
+    rows_to_ir(first->dense, dim, *first);
+  }
 }
 
 bool phase_type(const PGate& g) { return g.kind == GK::DIAG1 && popc(g.cmask) <= 1; }
@@ -378,6 +419,7 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates) {
       gi = gj;
     }
     d.n_prun = (uint32_t)n_prun;
+    factor_pass_scalars(pp);
     if (!pp.subs.empty()) plan.passes.push_back(std::move(pp));
     remaining.swap(deferred);
   }
