@@ -113,6 +113,13 @@ __device__ __forceinline__ void qc_compute_bar() {
   asm volatile("barrier.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / kGroupThreads), "n"(kGroupThreads)
                : "memory");
 }
+// Programmatic dependent launch (no-ops when the launch did not opt in): the
+// next pass's CTAs are launched while this one drains and do their setup; only
+// the producer warp touches global memory, and it waits for the previous grid
+// (complete + flushed) before its first load.
+__device__ __forceinline__ void qc_grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void qc_grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t qc_gtid() { return threadIdx.x % kGroupThreads; }
 __device__ __forceinline__ uint32_t qc_ins0(uint32_t x, int p) {
   return ((x >> p) << (p + 1)) | (x & ((1u << p) - 1u));
@@ -353,6 +360,8 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     qc_fence_mbar_init();
   }
   __syncthreads();
+  // every CTA of this grid is resident (grid <= SMs): the next pass may launch
+  qc_grid_dep_launch();
 
   const uint64_t n_tiles = pd.n_tiles;
   const uint64_t my_n =
@@ -363,6 +372,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     const int lane = tid & 31;
     const uint32_t row_bytes = row_amps * (uint32_t)sizeof(C);
     const uint32_t tile_bytes = nrows * row_bytes;
+    qc_grid_dep_wait();
     for (uint64_t i = 0; i < my_n + NBUF; ++i) {
       const int b = (int)(i % NBUF);
       C* buf = bufs + (size_t)b * buf_amps;

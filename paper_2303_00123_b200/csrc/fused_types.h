@@ -16,7 +16,10 @@ namespace qc {
 
 constexpr int kSlotBits = 4;          // 16 amplitudes per thread task
 constexpr int kSlots = 1 << kSlotBits;
-constexpr int kComputeWarps = 8;      // fused kernel: 8 compute warps ...
+#ifndef QC_COMPUTE_WARPS
+#define QC_COMPUTE_WARPS 8
+#endif
+constexpr int kComputeWarps = QC_COMPUTE_WARPS;  // fused kernel: compute warps ...
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kFusedThreads = kComputeThreads + 32;  // ... + 1 TMA producer warp
 // Compute warps form kGroups groups that take alternate tiles.  With NBUF not

@@ -264,8 +264,13 @@ void emit_run(const std::vector<PGate>& seq, size_t i, size_t j, int base, const
       t.d0 = 1;
       t.d1 = g.m[1];
     }
-    if (ctrl >= 0 && c.src(ctrl) == S_SLOT) {  // per-slot control: keep as its own op
+    if (ctrl >= 0 && c.src(ctrl) == S_SLOT) {  // per-slot control: own op + slot term
       extra.push_back(convert(g, c));
+      extra.back().folded = true;
+      t.src = S_SLOT;
+      t.bit = (uint8_t)c.slot(ctrl);
+      t.val = cval;
+      run.sterms.push_back(t);
       continue;
     }
     if (!is1(t.d0)) any0 = true;
@@ -295,6 +300,8 @@ void emit_run(const std::vector<PGate>& seq, size_t i, size_t j, int base, const
     run.terms.insert(run.terms.end(), outer.begin(), outer.end());
     run.terms.insert(run.terms.end(), none.begin(), none.end());
     out.push_back(run);
+  } else {
+    for (auto& e : extra) e.folded = false;  // no run to fold them into
   }
   for (auto& e : extra) out.push_back(e);
 }

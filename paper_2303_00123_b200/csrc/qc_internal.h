@@ -65,6 +65,11 @@ struct FOpIR {
   std::vector<cd> coefs;     // M1/M2: non-zero entries, row-major; DSCALE: d0, d1
   struct Term { uint8_t src, bit, val; cd d0, d1; };
   std::vector<Term> terms;   // PRUN, ordered local, outer, none
+  // PRUN: terms whose control is a slot bit (bit = slot index).  Their gates
+  // also follow the run as ordinary ops marked `folded`: the interpreter runs
+  // those, the JIT multiplies the slot terms into the run's per-slot factors.
+  std::vector<Term> sterms;
+  bool folded = false;
   cd dense[16];              // M1/M2: the exact matrix (row-major), for code generation
 };
 
