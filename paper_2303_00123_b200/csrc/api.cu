@@ -805,6 +805,12 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   if (blocks.empty()) return QC_OK;
   FusedPlan fp = plan_fused(n, k, rb, blocks);
   if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
+  // mirror build_fused_entry's layout choice (make_row_tmap's gather4 limits)
+  const bool g4 = ((uint64_t)(dbl ? 16 : 8) << rb) <= 1024 && n - rb <= 31 && n - rb >= 2;
+  for (auto& pp : fp.passes) {
+    pp.desc.g4 = g4 ? 1 : 0;
+    pp.desc.pshift = g4 ? 31 : rb;
+  }
   out->passes = (int64_t)fp.passes.size();
   for (auto& pp : fp.passes) {
     out->substages += (int64_t)pp.subs.size();

@@ -307,6 +307,13 @@ __device__ __forceinline__ void qc_scale_slots(C (&v)[kSlots], const C w, uint32
     if ((s & sm) == sv) v[s] = qc_cmul(w, v[s]);
 }
 // Phase run with its base bit on slot bit B: |1> slots x w1, |0> slots x w0.
+template <typename C>
+__device__ __forceinline__ void qc_swap(C& a, C& b) {
+  const C t = a;
+  a = b;
+  b = t;
+}
+
 template <int B, typename C>
 __device__ __forceinline__ void qc_prun_slot(C (&v)[kSlots], const C w0, const C w1, bool any0) {
 #pragma unroll
