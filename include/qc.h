@@ -105,8 +105,11 @@ typedef enum {
     QC_OPT_JIT = 6,           /* 1 (default): specialise repeated fused plans with NVRTC;
                                  0: never (AOT interpreting kernel); 2: from the first run  */
     QC_OPT_ROW_BITS = 7,      /* 0 (default): auto; else contiguous row bits of a fused tile */
-    QC_OPT_TMA_MODE = 8       /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
+    QC_OPT_TMA_MODE = 8,      /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
                                  request); 1: one cp.async.bulk per row                      */
+    QC_OPT_REMAP = 9          /* 1 (default): a fused pass may end by swapping row bits with
+                                 tile bits the next pass needs (a relabel, like SWAP);
+                                 0: the row bits keep their qubits                           */
 } qc_option;
 
 /* Counters of the most recent qc_run_circuit / qc_apply_gate. */

@@ -27,11 +27,14 @@ typedef struct qc_plan_stats {
     int64_t blob_bytes;   /* packed op blob bytes                           */
     int32_t tile_bits;
     int32_t jit_compiled; /* passes compiled by NVRTC (compile_jit != 0)    */
+    int64_t remap_swaps;  /* row-bit <-> tile-bit remap swaps (remap != 0)  */
+    int64_t restore_passes; /* swap-only passes restoring the input layout  */
 } qc_plan_stats;
 
-/* tile_bits / row_bits 0 = default.  errbuf (may be NULL) receives a message on error. */
+/* tile_bits / row_bits 0 = default; remap as QC_OPT_REMAP.  errbuf (may be
+ * NULL) receives a message on error. */
 qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
-                        int row_bits, int block_fusion, int compile_jit, qc_plan_stats* out,
+                        int row_bits, int block_fusion, int remap, int compile_jit, qc_plan_stats* out,
                         char* errbuf, size_t errlen);
 
 /* Sharded-state exchange arithmetic (host only): the runs of local indices

@@ -166,7 +166,7 @@ void plan_geometry(const qc_state* s, int n_plan, int* k_out, int* rb_out, int* 
 // controls / diagonal bits).  `tmap_base` / `tmap_bits`: the buffer and index
 // width the row tensor map spans.
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
-                            PlanEntry* e, void* tmap_base, int tmap_bits) {
+                            PlanEntry* e, void* tmap_base, int tmap_bits, bool remap) {
   int k, rb, ctas;
   plan_geometry(s, n_plan, &k, &rb, &ctas);
   e->ctas = ctas;
@@ -174,8 +174,9 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
   e->fused_gates = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  FusedPlan fp = plan_fused(n_plan, k, rb, blocks);
+  FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap);
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
+  e->perm = fp.perm;
   const bool g4 = s->tma_mode == 0 && make_row_tmap(tmap_base ? tmap_base : s->d, tmap_bits ? tmap_bits : n_plan, rb,
                                                      s->dbl, &e->tmap);
   for (auto& p : fp.passes) {
@@ -199,7 +200,7 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   int k, rb, ctas;
   plan_geometry(s, n, &k, &rb, &ctas);
   const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
-                        ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)(s->jit == 2) << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^
+                        ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)(s->jit == 2) << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^ ((uint64_t)s->remap << 52) ^
                         ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
   const uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
   auto it = s->plans.find(key);
@@ -229,11 +230,13 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
     g.src_op = (int)i;
     gates.push_back(g);
   }
-  e->layout_out.assign(lay, lay + n);
   if (!gates.empty()) {
-    const qc_status bs = build_fused_entry(s, gates, n, ~0ull, e.get());
+    const qc_status bs = build_fused_entry(s, gates, n, ~0ull, e.get(), nullptr, 0, s->remap != 0);
     if (bs != QC_OK) return bs;
+    if (!e->perm.empty())  // remap swaps moved physical bits: the layout follows the data
+      for (int q = 0; q < n; ++q) lay[q] = e->perm[lay[q]];
   }
+  e->layout_out.assign(lay, lay + n);
   PlanEntry* raw = e.get();
   if (s->plans.size() > 64) s->plans.clear();
   s->plans[key] = std::move(e);
@@ -730,6 +733,7 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       if (v < 0 || v > 1) return fail(QC_ERR_INVALID_ARG, "tma mode must be 0 or 1");
       s->tma_mode = (int)v;
       break;
+    case QC_OPT_REMAP: s->remap = v != 0; break;
     case QC_OPT_JIT:
       if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "jit must be 0, 1 or 2");
       s->jit = (int)v;
@@ -767,7 +771,7 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
 }  // extern "C"
 
 extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, size_t n_ops, int tile_bits,
-                                   int row_bits, int block_fusion, int compile_jit, qc_plan_stats* out,
+                                   int row_bits, int block_fusion, int remap, int compile_jit, qc_plan_stats* out,
                                    char* errbuf, size_t errlen) {
   auto err = [&](qc_status st, const std::string& m) {
     fail(st, "%s", m.c_str());
@@ -803,8 +807,10 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates, ~0ull) : gates;
   out->blocks = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  FusedPlan fp = plan_fused(n, k, rb, blocks);
+  FusedPlan fp = plan_fused(n, k, rb, blocks, remap != 0);
   if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
+  out->remap_swaps = fp.remap_swaps;
+  out->restore_passes = fp.restore_passes;
   // mirror build_fused_entry's layout choice (make_row_tmap's gather4 limits)
   const bool g4 = ((uint64_t)(dbl ? 16 : 8) << rb) <= 1024 && n - rb <= 31 && n - rb >= 2;
   for (auto& pp : fp.passes) {

@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "qc_internal.h"
@@ -330,13 +332,282 @@ void encode_substage(const std::vector<PGate>& seq, const Ctx& c, int& n_prun,
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates) {
+namespace {
+
+// Relabel physical bits a <-> b in a gate (the data of the two bits was swapped).
+void swap_bits(PGate& g, int a, int b) {
+  auto mv = [&](int p) { return p == a ? b : (p == b ? a : p); };
+  g.t0 = mv(g.t0);
+  if (pgate_is_two(g)) g.t1 = mv(g.t1);
+  auto mvmask = [&](uint64_t m) {
+    const uint64_t ba = (m >> a) & 1ull, bb = (m >> b) & 1ull;
+    m &= ~((1ull << a) | (1ull << b));
+    return m | (ba << b) | (bb << a);
+  };
+  g.cmask = mvmask(g.cmask);
+  g.cval = mvmask(g.cval);
+}
+
+// Bits the next pass's greedy would want in its tile if all k tile bits were
+// free (the row bits not reserved): the needed bits of the gates it would take.
+uint64_t next_want(const std::vector<PGate>& gates, const std::vector<int>& rem, int k) {
+  uint64_t W = 0, blocked = 0;
+  for (int gi : rem) {
+    const PGate& g = gates[gi];
+    const uint64_t all = pgate_bits(g);
+    if (all & blocked) {
+      blocked |= all;
+      continue;
+    }
+    const uint64_t nw = W | need_mask(g);
+    if (popc(nw) <= k) W = nw;
+    else blocked |= all;
+  }
+  return W;
+}
+
+struct Group {
+  std::vector<PGate> gates;
+  uint64_t G = 0;
+};
+
+// Non-diagonal gates a pass with tile set T would take from `rem` (in order;
+// a gate is taken iff its non-diagonal targets lie in T and no earlier
+// deferred gate shares a bit with it).  Stops once every bit of T is blocked.
+int score_tile(const std::vector<PGate>& gates, const std::vector<int>& rem, uint64_t T) {
+  uint64_t blocked = 0;
+  int sc = 0;
+  for (int gi : rem) {
+    const PGate& g = gates[gi];
+    const uint64_t all = pgate_bits(g);
+    const uint64_t nd = need_mask(g);
+    if (!(all & blocked) && (nd & ~T) == 0) {
+      sc += nd != 0;
+      continue;
+    }
+    blocked |= all;
+    if ((blocked & T) == T) break;
+  }
+  return sc;
+}
+
+// Tile set for the next pass: in-order greedy growth from `fixed`, then hill
+// climbing over single-bit exchanges (bits of `fixed` stay) on score_tile.
+uint64_t choose_tile(const std::vector<PGate>& gates, const std::vector<int>& rem, uint64_t fixed, int k, int n) {
+  uint64_t T = fixed, blocked = 0;
+  for (int gi : rem) {
+    const PGate& g = gates[gi];
+    const uint64_t all = pgate_bits(g);
+    if (all & blocked) {
+      blocked |= all;
+      continue;
+    }
+    const uint64_t nt = T | need_mask(g);
+    if (popc(nt) <= k) T = nt;
+    else blocked |= all;
+  }
+  const uint64_t full = n >= 64 ? ~0ull : (1ull << n) - 1;
+  int best = score_tile(gates, rem, T);
+  for (int it = 0; it < 64; ++it) {
+    uint64_t bestT = 0;
+    const uint64_t outs = full & ~T;
+    if (popc(T) < k) {
+      for (uint64_t o = outs; o; o &= o - 1) {
+        const uint64_t t2 = T | (o & -o);
+        const int sc = score_tile(gates, rem, t2);
+        if (sc > best) best = sc, bestT = t2;
+      }
+    } else {
+      for (uint64_t i = T & ~fixed; i; i &= i - 1)
+        for (uint64_t o = outs; o; o &= o - 1) {
+          const uint64_t t2 = (T & ~(i & -i)) | (o & -o);
+          const int sc = score_tile(gates, rem, t2);
+          if (sc > best) best = sc, bestT = t2;
+        }
+    }
+    if (!bestT) break;
+    T = bestT;
+  }
+  return T;
+}
+
+}  // namespace
+
+namespace {
+
+// Each swap joins the first group at or after the last one touching its bits
+// that has slot room; else a new trailing group (order of swaps sharing a bit
+// is kept: earlier ones count as touching).
+void place_swaps(std::vector<Group>& groups, const std::vector<std::pair<int, int>>& swaps) {
+  for (auto [a, b] : swaps) {
+    const uint64_t ab = (1ull << a) | (1ull << b);
+    size_t j = 0;
+    for (size_t x = 0; x < groups.size(); ++x)
+      for (const PGate& g : groups[x].gates)
+        if (pgate_bits(g) & ab) j = x;
+    PGate sw;
+    sw.kind = GK::SWAP2;
+    sw.t0 = std::max(a, b);
+    sw.t1 = std::min(a, b);
+    size_t x = j;
+    while (x < groups.size() && popc(groups[x].G | ab) > kSlotBits) ++x;
+    if (x == groups.size()) groups.emplace_back();
+    groups[x].G |= ab;
+    groups[x].gates.push_back(sw);
+  }
+}
+
+// Encode one pass over tile set T from its sub-stage groups.
+void emit_pass(int n, int k, int rb, uint64_t T, const std::vector<Group>& groups, FusedPlan& plan) {
+  FusedPassPlan pp{};
+  const Frame f = make_frame(n, rb, T);
+  PassDesc& d = pp.desc;
+  d.k = k;
+  d.rb = rb;
+  d.pshift = rb;
+  d.g4 = 0;
+  d.rank_bits = 0;
+  d.addr_bits = 0;
+  d.n_hi = 0;
+  for (int p = rb; p < n; ++p)
+    if (T & (1ull << p)) d.hi_pos[d.n_hi++] = p;
+  d.n_outer = 0;
+  for (int p = 0; p < n; ++p)
+    if (!(T & (1ull << p))) d.outer_pos[d.n_outer++] = p;
+  d.n_tiles = 1ull << (n - k);
+  int n_prun = 0;
+  for (const Group& gr : groups) {
+    const uint64_t G = gr.G;
+    // pad G with the highest tile-local bits (lanes then walk contiguous rows)
+    bool in_g[64] = {false};
+    for (int p = 0; p < n; ++p)
+      if (G & (1ull << p)) in_g[f.local_of[p]] = true;
+    int cnt = popc(G);
+    for (int l = f.n_local - 1; l >= 0 && cnt < kSlotBits; --l) {
+      if (in_g[l]) continue;
+      in_g[l] = true;
+      ++cnt;
+    }
+    SubStageDesc sd{};
+    Ctx c;
+    c.f = &f;
+    for (int l = 0; l < 64; ++l) c.slot_of_local[l] = -1;
+    int j = 0;
+    for (int l = 0; l < f.n_local; ++l)
+      if (in_g[l]) {
+        sd.g[j] = l;
+        c.slot_of_local[l] = j++;
+      }
+    sd.op_begin = (int)pp.ops.size();
+    encode_substage(gr.gates, c, n_prun, pp.ops);
+    sd.op_end = (int)pp.ops.size();
+    if (sd.op_end > sd.op_begin) pp.subs.push_back(sd);
+  }
+  d.n_prun = (uint32_t)n_prun;
+  factor_pass_scalars(pp);
+  if (!pp.subs.empty()) plan.passes.push_back(std::move(pp));
+}
+
+// Swaps (applied in order) that move the data of every physical bit back
+// home: perm[p] = where the data of home p currently is.
+std::vector<std::pair<int, int>> restore_swaps(std::vector<int> cur) {
+  std::vector<std::pair<int, int>> out;
+  const int n = (int)cur.size();
+  std::vector<int> home_at(n);  // home_at[pos] = home whose data is at pos
+  for (int h = 0; h < n; ++h) home_at[cur[h]] = h;
+  for (int p = 0; p < n; ++p) {
+    if (cur[p] == p) continue;
+    const int q = cur[p], h = home_at[p];  // p's data at q; position p holds h's data
+    out.push_back({p, q});
+    cur[p] = p;
+    home_at[p] = p;
+    cur[h] = q;
+    home_at[q] = h;
+  }
+  return out;
+}
+
+// End-of-pass permutation of the tile's bits (remap).  Row positions get
+// items (the data of a home bit) the next pass wants, preferring items whose
+// home is that row; the other tile positions send items home where possible;
+// everything else stays.  Returned as swaps applied in order.
+std::vector<std::pair<int, int>> remap_swaps(const std::vector<int>& perm, uint64_t T, uint64_t rows, uint64_t W,
+                                             int n) {
+  std::vector<int> home_at(n);
+  for (int h = 0; h < n; ++h) home_at[perm[h]] = h;
+  std::vector<int> want(n, -1);  // target position -> item (home index)
+  std::vector<char> placed(n, 0);
+  auto in = [](uint64_t m, int p) { return (m >> p) & 1ull; };
+  if (W) {  // W == 0: plain restore, rows are ordinary tile positions
+    // rows: wanted items whose home is the row, then wanted items already in a row, then others
+    for (int r = 0; r < n; ++r)
+      if (in(rows, r) && in(T, perm[r]) && in(W, perm[r])) {
+        want[r] = r;
+        placed[r] = 1;
+      }
+    for (int r = 0; r < n; ++r)
+      if (in(rows, r) && want[r] < 0) {
+        const int it = home_at[r];
+        if (!placed[it] && in(W, r)) want[r] = it, placed[it] = 1;
+      }
+    for (int r = 0; r < n; ++r) {
+      if (!in(rows, r) || want[r] >= 0) continue;
+      for (int p = 0; p < n; ++p) {
+        const int it = home_at[p];
+        if (in(T, p) && !in(rows, p) && in(W, p) && !placed[it]) {
+          want[r] = it, placed[it] = 1;
+          break;
+        }
+      }
+    }
+    for (int r = 0; r < n; ++r)  // unwanted rows: keep the occupant if free
+      if (in(rows, r) && want[r] < 0 && !placed[home_at[r]]) want[r] = home_at[r], placed[home_at[r]] = 1;
+  }
+  // other tile positions: items going home, then occupants staying
+  for (int p = 0; p < n; ++p)
+    if (in(T, p) && (!W || !in(rows, p)) && want[p] < 0 && in(T, perm[p]) && !placed[p]) want[p] = p, placed[p] = 1;
+  for (int p = 0; p < n; ++p)
+    if (in(T, p) && want[p] < 0 && !placed[home_at[p]]) want[p] = home_at[p], placed[home_at[p]] = 1;
+  for (int p = 0; p < n; ++p) {
+    if (!in(T, p) || want[p] >= 0) continue;
+    for (int q = 0; q < n; ++q)
+      if (in(T, q) && !placed[home_at[q]]) {
+        want[p] = home_at[q], placed[home_at[q]] = 1;
+        break;
+      }
+  }
+  // decompose: position p must receive item want[p] (currently at pos[want[p]])
+  std::vector<int> pos(perm);
+  std::vector<std::pair<int, int>> out;
+  for (int p = 0; p < n; ++p) {
+    if (!in(T, p) || want[p] < 0) continue;
+    const int q = pos[want[p]];
+    if (q == p) continue;
+    const int other = home_at[p];
+    out.push_back({p, q});
+    pos[want[p]] = p;
+    home_at[p] = want[p];
+    pos[other] = q;
+    home_at[q] = other;
+  }
+  return out;
+}
+
+}  // namespace
+
+FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, bool remap) {
   FusedPlan plan;
+  std::vector<PGate> gates = gates_in;  // bits relabelled by in-pass remap swaps
+  plan.perm.resize(n);
+  for (int p = 0; p < n; ++p) plan.perm[p] = p;
+  const uint64_t rows = (1ull << rb) - 1;
   std::vector<int> remaining(gates.size());
   for (size_t i = 0; i < gates.size(); ++i) remaining[i] = (int)i;
 
   while (!remaining.empty()) {
-    uint64_t T = (1ull << rb) - 1;
+    // search: the tile set is fixed before the take scan (row bits always in it)
+    const uint64_t Tc = (remap && n > k) ? choose_tile(gates, remaining, rows, k, n) : ~0ull;
+    uint64_t T = rows;
     uint64_t blocked = 0;
     size_t bytes = 0;
     std::vector<int> taken, deferred;
@@ -347,7 +618,7 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates) {
         return plan;
       }
       const uint64_t all = pgate_bits(g);
-      if (all & blocked) {
+      if ((all & blocked) || (need_mask(g) & ~Tc)) {
         blocked |= all;
         deferred.push_back(gi);
         continue;
@@ -367,69 +638,96 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates) {
       plan.ok = false;
       return plan;
     }
+    // Remap (n > k): the row bits are in every tile, so whichever qubits sit
+    // there ride along in every pass.  Swap row bits the next pass does not
+    // want with tile bits it does want -- a permutation of this tile's bits,
+    // appended after this pass's last gate on those bits (register renaming
+    // inside a sub-stage) -- and relabel the deferred gates accordingly.
+    std::vector<std::pair<int, int>> swaps;
+    uint64_t W = 0;
+    if (remap && n > k && !deferred.empty()) W = choose_tile(gates, deferred, 0, k, n);
+    // last pass: bring every displaced bit home (same layout in and out, so a
+    // repeated circuit reuses its plan, JIT kernels and CUDA graph)
+    uint64_t D = 0;  // displaced positions (padding with them lets items go home)
+    if (remap)
+      for (int p = 0; p < n; ++p)
+        if (plan.perm[p] != p) D |= 1ull << p;
+    for (int p = rb; popc(T) < k && p < n; ++p)  // pad: displaced / wanted bits first
+      if ((D | W) & (1ull << p)) T |= 1ull << p;
     for (int p = rb; popc(T) < k && p < n; ++p) T |= 1ull << p;
-
-    FusedPassPlan pp{};
-    const Frame f = make_frame(n, rb, T);
-    PassDesc& d = pp.desc;
-    d.k = k;
-    d.rb = rb;
-    d.pshift = rb;
-    d.g4 = 0;
-    d.rank_bits = 0;
-    d.addr_bits = 0;
-    d.n_hi = 0;
-    for (int p = rb; p < n; ++p)
-      if (T & (1ull << p)) d.hi_pos[d.n_hi++] = p;
-    d.n_outer = 0;
-    for (int p = 0; p < n; ++p)
-      if (!(T & (1ull << p))) d.outer_pos[d.n_outer++] = p;
-    d.n_tiles = 1ull << (n - k);
-    int n_prun = 0;
-
-    size_t gi = 0;
-    while (gi < taken.size()) {
-      uint64_t G = 0;
+    if (deferred.empty() && D && (D & ~T) == 0) swaps = restore_swaps(plan.perm);
+    else if (W || (deferred.empty() && D)) swaps = remap_swaps(plan.perm, T, rows, W, n);
+    // sub-stage groups: consecutive gates whose non-diagonal targets fit kSlotBits
+    std::vector<Group> groups;
+    for (size_t gi = 0; gi < taken.size();) {
+      Group gr;
       size_t gj = gi;
       while (gj < taken.size()) {
-        const uint64_t ng = G | need_mask(gates[taken[gj]]);
+        const uint64_t ng = gr.G | need_mask(gates[taken[gj]]);
         if (popc(ng) > kSlotBits) break;
-        G = ng;
+        gr.G = ng;
+        gr.gates.push_back(gates[taken[gj]]);
         ++gj;
       }
-      // pad G with the highest tile-local bits (lanes then walk contiguous rows)
-      bool in_g[64] = {false};
-      for (int p = 0; p < n; ++p)
-        if (G & (1ull << p)) in_g[f.local_of[p]] = true;
-      int cnt = popc(G);
-      for (int l = f.n_local - 1; l >= 0 && cnt < kSlotBits; --l) {
-        if (in_g[l]) continue;
-        in_g[l] = true;
-        ++cnt;
-      }
-      SubStageDesc sd{};
-      Ctx c;
-      c.f = &f;
-      for (int l = 0; l < 64; ++l) c.slot_of_local[l] = -1;
-      int j = 0;
-      for (int l = 0; l < f.n_local; ++l)
-        if (in_g[l]) {
-          sd.g[j] = l;
-          c.slot_of_local[l] = j++;
-        }
-      std::vector<PGate> seq;
-      for (size_t x = gi; x < gj; ++x) seq.push_back(gates[taken[x]]);
-      sd.op_begin = (int)pp.ops.size();
-      encode_substage(seq, c, n_prun, pp.ops);
-      sd.op_end = (int)pp.ops.size();
-      if (sd.op_end > sd.op_begin) pp.subs.push_back(sd);
+      groups.push_back(std::move(gr));
       gi = gj;
     }
-    d.n_prun = (uint32_t)n_prun;
-    factor_pass_scalars(pp);
-    if (!pp.subs.empty()) plan.passes.push_back(std::move(pp));
+    place_swaps(groups, swaps);
+    emit_pass(n, k, rb, T, groups, plan);
+    for (auto [a, b] : swaps) {
+      for (int gi : deferred) swap_bits(gates[gi], a, b);
+      for (int p = 0; p < n; ++p)
+        plan.perm[p] = plan.perm[p] == a ? b : (plan.perm[p] == b ? a : plan.perm[p]);
+    }
+    plan.remap_swaps += (int64_t)swaps.size();
     remaining.swap(deferred);
   }
+  // displaced bits the last tile did not hold: swap-only passes.  Item moves
+  // (position -> home) form cycles; a tile fixes every move whose two ends it
+  // holds, so each pass grows T from the row bits by the position closing
+  // the most moves.
+  if (getenv("QC_PLAN_DEBUG")) {
+    int nd = 0;
+    for (int p = 0; p < n; ++p) nd += plan.perm[p] != p;
+    fprintf(stderr, "plan: %zu passes, %d displaced bits\n", plan.passes.size(), nd);
+  }
+  for (int guard = 0; guard < 64; ++guard) {
+    std::vector<int> home_at(n);
+    for (int h = 0; h < n; ++h) home_at[plan.perm[h]] = h;
+    uint64_t D = 0;
+    for (int p = 0; p < n; ++p)
+      if (plan.perm[p] != p) D |= 1ull << p;
+    if (!D) break;
+    uint64_t T = rows;
+    auto edges = [&](uint64_t t) {  // moves with both ends in t
+      int e = 0;
+      for (int p = 0; p < n; ++p)
+        if (((D >> p) & 1) && ((t >> p) & 1) && ((t >> home_at[p]) & 1)) ++e;
+      return e;
+    };
+    while (popc(T) < k && (D & ~T)) {
+      int bestp = -1, beste = -1;
+      for (uint64_t o = D & ~T; o; o &= o - 1) {
+        const int p = std::countr_zero(o);
+        const int e = edges(T | (1ull << p));
+        if (e > beste) beste = e, bestp = p;
+      }
+      T |= 1ull << bestp;
+    }
+    for (int p = rb; popc(T) < k && p < n; ++p) T |= 1ull << p;
+    const std::vector<std::pair<int, int>> chunk = remap_swaps(plan.perm, T, rows, 0, n);
+    if (chunk.empty()) break;
+    std::vector<Group> groups;
+    place_swaps(groups, chunk);
+    emit_pass(n, k, rb, T, groups, plan);
+    for (auto [a, b] : chunk)
+      for (int p = 0; p < n; ++p)
+        plan.perm[p] = plan.perm[p] == a ? b : (plan.perm[p] == b ? a : plan.perm[p]);
+    plan.remap_swaps += (int64_t)chunk.size();
+    ++plan.restore_passes;
+  }
+  for (int p = 0; p < n; ++p)
+    if (plan.perm[p] != p) plan.ok = false;  // (cannot happen: every pass fixes >= 1 move)
   return plan;
 }
 

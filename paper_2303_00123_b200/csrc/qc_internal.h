@@ -82,10 +82,15 @@ struct FusedPassPlan {
 struct FusedPlan {
   bool ok = true;
   std::vector<FusedPassPlan> passes;
+  // remap: the data of physical bit p ends at physical bit perm[p]
+  std::vector<int> perm;
+  int64_t remap_swaps = 0;
+  int64_t restore_passes = 0;  // swap-only passes that restore the input layout
 };
 
 // Planner (plan.cpp).  k = tile bits (<= n), returns passes covering all gates.
-FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates);
+// remap: passes may end with swaps of row bits and tile bits (plan.perm).
+FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates, bool remap = false);
 // Pack the plan into one device blob for precision T (fills desc.blob_*).
 std::vector<uint8_t> pack_plan(FusedPlan& plan, bool dbl);
 

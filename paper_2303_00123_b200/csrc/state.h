@@ -29,6 +29,7 @@ struct PlanEntry {
   cudaGraphExec_t exec = nullptr;
   int ctas = 0;
   int tile_bits = 0;
+  std::vector<int> perm;             // remap: data of physical bit p ends at perm[p]
   ~PlanEntry() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -47,7 +48,7 @@ PGate lower(const qc_gate& g, const int* layout);
 qc_status validate_gate(int n, const qc_gate& g, size_t idx);
 uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt);
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
-                            PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0);
+                            PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0, bool remap = false);
 int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
                   uint64_t addr_bits);
 qc_status maybe_jit(qc_state* s, PlanEntry* e);
@@ -91,6 +92,7 @@ struct qc_state {
   // options
   int fusion = 1, relabel = 1, use_graph = 1, tile_bits = 0, ctas = 0, block_fusion = 1, jit = 1;
   int row_bits = 0, tma_mode = 0;
+  int remap = 1;  // QC_OPT_REMAP
   std::string jit_error;
   // stats
   int64_t last_gates = 0, last_passes = 0, last_launches = 0, last_relabels = 0;

@@ -29,7 +29,7 @@ ARITY = {"H": 1, "X": 1, "Y": 1, "Z": 1, "P": 1, "RX": 1, "RY": 1, "RZ": 1, "CNO
 QC_CTRL_ONES = 0xFFFFFFFF
 OPTIONS = {"fusion": 0, "relabel_swap": 1, "use_graph": 2, "tile_bits": 3, "ctas": 4,
            "block_fusion": 5, "jit": 6, "row_bits": 7,
-           "tma_mode": 8}
+           "tma_mode": 8, "remap": 9}
 
 GATE_DTYPE = np.dtype([("op", "<i4"), ("qubits", "<i4", (3,)), ("ctrl_state", "<u4"),
                        ("flags", "<u4"), ("theta", "<f8"), ("m", "<f8", (32,))])
@@ -65,7 +65,8 @@ class qc_plan_stats(ctypes.Structure):
                 ("passes", ctypes.c_int64), ("substages", ctypes.c_int64),
                 ("fused_ops", ctypes.c_int64), ("phase_runs", ctypes.c_int64),
                 ("blob_bytes", ctypes.c_int64), ("tile_bits", ctypes.c_int32),
-                ("jit_compiled", ctypes.c_int32)]
+                ("jit_compiled", ctypes.c_int32), ("remap_swaps", ctypes.c_int64),
+                ("restore_passes", ctypes.c_int64)]
 
 
 DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange"]
@@ -99,7 +100,7 @@ def lib() -> ctypes.CDLL:
     L.qc_state_norm2.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     L.qc_set_option.argtypes = [vp, i32, ctypes.c_int64]
     L.qc_get_info.argtypes = [vp, ctypes.POINTER(qc_info)]
-    L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
+    L.qc_debug_plan.argtypes = [i32, i32, vp, sz, i32, i32, i32, i32, i32, ctypes.POINTER(qc_plan_stats),
                                 ctypes.c_char_p, sz]
     L.qc_debug_plan.restype = ctypes.c_int
     L.qc_state_create_dist.argtypes = [i32, i32, i32, i32, vp, ctypes.POINTER(vp)]
@@ -286,7 +287,7 @@ class State:
 
 
 def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_fusion: bool = True,
-               compile_jit: bool = False, row_bits: int = 0) -> dict:
+               compile_jit: bool = False, row_bits: int = 0, remap: bool = True) -> dict:
     """Plan an op list on the host (no GPU) and report its shape; optionally
     NVRTC-compile every pass's specialised kernel (qc_debug.h)."""
     arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
@@ -294,7 +295,8 @@ def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_f
     st = qc_plan_stats()
     eb = ctypes.create_string_buffer(4096)
     rc = lib().qc_debug_plan(n, PRECISION[precision], arr.ctypes.data if len(arr) else None, len(arr),
-                             tile_bits, row_bits, int(block_fusion), int(compile_jit), ctypes.byref(st),
+                             tile_bits, row_bits, int(block_fusion), int(remap), int(compile_jit),
+                             ctypes.byref(st),
                              eb, 4096)
     if rc != QC_OK:
         raise QCError(rc, eb.value.decode())

@@ -343,3 +343,37 @@ def test_repeated_runs_roundtrip(qcmod, n, prec, rb):
         assert abs(s.norm2() - n0) <= (1e-9 if prec == "c128" else 1e-4) * n0
     ref = qcgen.random_state(n, seed=3, precision=prec)[: 1 << 12]
     assert maxerr(got, ref) <= TOL[prec] * 10
+
+
+# ---------------------------------------------------------- remap (row-bit relabelling between passes)
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("n,tile_bits,circ", [(16, 0, "tfxy"), (18, 9, "tfxy"), (17, 8, "random"),
+                                              (20, 0, "random"), (15, 7, "qft")])
+def test_remap_matches_oracle_and_restores_layout(qcmod, prec, n, tile_bits, circ):
+    """Passes that end by swapping row bits with tile bits (QC_OPT_REMAP) give
+    the oracle's result, and the run leaves the layout it started with."""
+    ops = {"tfxy": lambda: qcgen.tfxy(n, 4), "qft": lambda: qcgen.qft(n),
+           "random": lambda: qcgen.random_circuit(n, 300, seed=900 + n)}[circ]()
+    ref = ref_run(n, prec, ops)
+    for jit in (0, 2):
+        with qcmod.State(n, prec) as s:
+            s.set_option("tile_bits", tile_bits)
+            s.set_option("jit", jit)
+            s.set_option("relabel_swap", 0)  # so the only relabelling is the remap
+            s.init_random(qcgen.STATE_SEED)
+            s.run(ops)
+            info = s.info()
+            got = s.read()
+        assert info["layout_is_canonical"], info
+        assert maxerr(got, ref) <= TOL[prec], (jit, maxerr(got, ref))
+    st = qcmod.qc.debug_plan(n, ops, precision=prec, tile_bits=tile_bits)
+    if circ != "qft":
+        assert st["remap_swaps"] > 0, st
+
+
+def test_remap_permutation_circuit_bit_exact(qcmod):
+    n = 18
+    ops = qcgen.random_circuit(n, 400, seed=78, kinds=("X", "CNOT", "SWAP", "CCX"))
+    for prec in ("c128", "c64"):
+        got, info = gpu_run(qcmod, n, prec, ops, tile_bits=8, jit=2)
+        assert np.array_equal(got.astype(np.complex128), ref_run(n, prec, ops))

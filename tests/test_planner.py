@@ -41,8 +41,9 @@ def test_every_gate_is_planned(n, tile):
     st = qc.debug_plan(n, ops, tile_bits=tile, block_fusion=False)
     nonswap = sum(1 for o in ops if o.name != "SWAP")
     assert st["blocks"] == nonswap
-    # every non-SWAP gate is encoded exactly once (phase runs absorb several)
-    assert st["fused_ops"] <= nonswap and st["fused_ops"] > 0
+    # every non-SWAP gate is encoded exactly once (phase runs absorb several);
+    # remap swaps are extra permutation ops
+    assert st["fused_ops"] <= nonswap + st["remap_swaps"] and st["fused_ops"] > 0
 
 
 def test_invalid_ops_rejected():
@@ -62,3 +63,23 @@ def test_jit_codegen_compiles_for_sm100a(prec):
     ops = qcgen.random_circuit(n, 120, seed=5) + qcgen.qft(n) + qcgen.tfxy(n, 2)
     st = qc.debug_plan(n, ops, precision=prec, tile_bits=10, compile_jit=True)
     assert st["jit_compiled"] == st["passes"] > 1
+
+
+@pytest.mark.parametrize("n,prec", [(20, "c128"), (28, "c128"), (33, "c128"), (30, "c64")])
+def test_remap_cuts_tfxy_passes(n, prec):
+    """Row-bit remap: the nearest-neighbour Trotter circuit needs far fewer
+    passes when the row bits may change qubits between passes; the plan ends
+    in the layout it started from (restore passes counted in `passes`)."""
+    ops = qcgen.tfxy(n, 10)
+    on = qc.debug_plan(n, ops, precision=prec)
+    off = qc.debug_plan(n, ops, precision=prec, remap=False)
+    assert off["remap_swaps"] == 0 and off["restore_passes"] == 0
+    assert on["remap_swaps"] > 0
+    assert on["passes"] * 2 <= off["passes"], (on, off)
+    assert on["restore_passes"] <= 3
+
+
+def test_remap_off_below_tile():
+    # whole state in one tile: no passes to remap between
+    st = qc.debug_plan(10, qcgen.tfxy(10, 10))
+    assert st["passes"] == 1 and st["remap_swaps"] == 0
