@@ -435,6 +435,66 @@ uint64_t choose_tile(const std::vector<PGate>& gates, const std::vector<int>& re
 
 namespace {
 
+// Sub-stage groups of one pass: list scheduling over the pass's gates (a
+// gate is ready once every earlier gate sharing a bit with it is placed).
+// A group first takes, lowest index first, every ready gate whose
+// non-diagonal targets already lie in its slot set G; then it grows G by the
+// ready gate adding the fewest bits (<= kSlotBits).  Gates keep their
+// relative order on every bit, so the product is unchanged; brickwork layers
+// fold into triangles of 3-4 blocks per 4-bit group instead of 2.
+std::vector<Group> form_groups(const std::vector<PGate>& seq) {
+  const int m = (int)seq.size();
+  std::vector<std::vector<int>> succ(m);
+  std::vector<int> npred(m, 0);
+  int last[64];
+  for (int b = 0; b < 64; ++b) last[b] = -1;
+  for (int j = 0; j < m; ++j) {
+    int preds[64], np = 0;
+    for (uint64_t x = pgate_bits(seq[j]); x; x &= x - 1) {
+      const int b = std::countr_zero(x);
+      if (last[b] >= 0 && std::find(preds, preds + np, last[b]) == preds + np) preds[np++] = last[b];
+      last[b] = j;
+    }
+    for (int i = 0; i < np; ++i) succ[preds[i]].push_back(j);
+    npred[j] = np;
+  }
+  std::vector<char> ready(m, 0), done(m, 0);
+  for (int j = 0; j < m; ++j) ready[j] = npred[j] == 0;
+  std::vector<Group> groups;
+  int left = m;
+  auto place = [&](Group& gr, int j) {
+    gr.G |= need_mask(seq[j]);
+    gr.gates.push_back(seq[j]);
+    done[j] = 1;
+    ready[j] = 0;
+    --left;
+    for (int s2 : succ[j])
+      if (--npred[s2] == 0) ready[s2] = 1;
+  };
+  while (left > 0) {
+    Group gr;
+    for (;;) {
+      int pick = -1;
+      for (int j = 0; j < m && pick < 0; ++j)
+        if (ready[j] && (need_mask(seq[j]) & ~gr.G) == 0) pick = j;
+      if (pick >= 0) {
+        place(gr, pick);
+        continue;
+      }
+      int best = kSlotBits + 1;
+      for (int j = 0; j < m; ++j) {
+        if (!ready[j]) continue;
+        const int c = popc(gr.G | need_mask(seq[j]));
+        if (c < best) best = c, pick = j;
+      }
+      if (pick < 0 || best > kSlotBits) break;
+      place(gr, pick);
+    }
+    groups.push_back(std::move(gr));
+  }
+  return groups;
+}
+
 // Each swap joins the first group at or after the last one touching its bits
 // that has slot room; else a new trailing group (order of swaps sharing a bit
 // is kept: earlier ones count as touching).
@@ -657,21 +717,10 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
     for (int p = rb; popc(T) < k && p < n; ++p) T |= 1ull << p;
     if (deferred.empty() && D && (D & ~T) == 0) swaps = restore_swaps(plan.perm);
     else if (W || (deferred.empty() && D)) swaps = remap_swaps(plan.perm, T, rows, W, n);
-    // sub-stage groups: consecutive gates whose non-diagonal targets fit kSlotBits
-    std::vector<Group> groups;
-    for (size_t gi = 0; gi < taken.size();) {
-      Group gr;
-      size_t gj = gi;
-      while (gj < taken.size()) {
-        const uint64_t ng = gr.G | need_mask(gates[taken[gj]]);
-        if (popc(ng) > kSlotBits) break;
-        gr.G = ng;
-        gr.gates.push_back(gates[taken[gj]]);
-        ++gj;
-      }
-      groups.push_back(std::move(gr));
-      gi = gj;
-    }
+    std::vector<PGate> seq;
+    seq.reserve(taken.size());
+    for (int gi : taken) seq.push_back(gates[gi]);
+    std::vector<Group> groups = form_groups(seq);
     place_swaps(groups, swaps);
     emit_pass(n, k, rb, T, groups, plan);
     for (auto [a, b] : swaps) {
