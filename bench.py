@@ -50,6 +50,28 @@ def build_ops(cfg, n=None):
     return qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, steps)
 
 
+# Algorithmic flops per amplitude of each unfused gate: dense
+# 1q 14, dense 2q 30, a diagonal factor 6 per touched amplitude, 0 for
+# permutations (X, CNOT, SWAP, CCX; Y and CZ are sign / i-multiples).
+FLOPS_PER_AMP = {"H": 14, "RX": 14, "RY": 14, "U1": 14, "RZ": 6, "P": 3, "CP": 1.5, "Z": 0, "CZ": 0,
+                 "Y": 0, "X": 0, "CNOT": 0, "SWAP": 0, "CCX": 0, "CU1": 7, "U2": 30}
+
+
+def circuit_flops(ops, n):
+    return float(sum(FLOPS_PER_AMP[o.name] for o in ops)) * float(1 << n)
+
+
+def load_traffic(cfg):
+    """dram read+write bytes per launch of qc_pass from the committed ncu
+    --set full capture of this workload (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f).get(cfg)
+        return (d["bytes_per_launch"], d["source"]) if d else (None, None)
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -212,10 +234,28 @@ def run_ours(args, rank, world, local_rank):
         e_ms = float(t.item())
 
     peak, peak_kind = load_peaks()
-    # dominant kernel = fused_pass_kernel (every launch of the step is one);
-    # algorithmic bytes per launch = read + write of the whole state (2*Ns).
+    # dominant kernel = the fused pass (every launch of the step is one).
+    # HBM view: algorithmic bytes per launch = read + write of the state (2*Ns).
+    # ALU view: algorithmic flops of the circuit's unfused gates
+    # per launch, against the FP64 (c128) / FP32 (c64) FMA peak measured on
+    # this GPU by qc_debug_fma_peak.  TFXY is bound by the FP64 pipe (block-
+    # fused pair blocks, ~8 FP64 instructions per amplitude each), QFT by HBM.
     avg_launch_ms = ms_per_step / max(launches_per_step, 1)
     achieved = 2 * state_bytes / (avg_launch_ms / 1e3) / 1e9
+    fma_peak = qc.qc.fma_peak(prec == "c128")
+    flops = circuit_flops(ops, n)
+    alu_achieved = flops / max(launches_per_step, 1) / (avg_launch_ms / 1e3) / 1e12
+    traffic, traffic_src = load_traffic(args.config)
+    hbm_view = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "bytes_per_launch": 2 * state_bytes}
+    alu_view = {"bound": "alu", "achieved": alu_achieved, "peak": fma_peak, "unit": "TFLOP/s",
+                "frac": alu_achieved / fma_peak,
+                "peak_source": f"measured {'FP64' if prec == 'c128' else 'FP32'} FMA peak (qc_debug_fma_peak, "
+                               "8 independent FMA chains/thread, this GPU, this run)",
+                "flops_per_launch": flops / max(launches_per_step, 1),
+                "flops_note": "algorithmic = unfused per-gate flops/amp (dense 1q 14, dense 2q 30, diagonal "
+                              "6 per touched amp, permutations 0) x 2^n, / fused launches per step"}
+    main_view = alu_view if fam == "tfxy" else hbm_view
     out = {
         "metric": METRIC, "value": value, "unit": "circuit/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -229,15 +269,11 @@ def run_ours(args, rank, world, local_rank):
                    "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"],
                    "jit_specialised": info["last_jit"], "ops_after_block_fusion": info["last_blocks"]},
         "gpu_launches": int(launches_per_step * args.steps),
-        "roofline": {"bound": "hbm", "kernel": "qc_pass (NVRTC-specialised fused tile pass)",
-                     "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "traffic": None,
-                     "bytes_per_launch": 2 * state_bytes,
-                     "avg_launch_ms": avg_launch_ms,
+        "roofline": {**main_view, "kernel": "qc_pass (NVRTC-specialised fused tile pass)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "avg_launch_ms": avg_launch_ms, "hbm_view": hbm_view, "alu_view": alu_view,
                      "note": "avg launch = timed step time / fused launches per step (every launch of "
-                             "the step is a fused pass); algorithmic bytes = read+write of the state"},
+                             "the step is a fused pass, timed by CUDA events on the state's stream)"},
         "e2e": {"value": world / (e_ms / 1e3), "unit": "circuit/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "ms_per_step": e_ms},
         "clocks": clocks,
@@ -357,7 +393,9 @@ def sweep(args, local_rank):
     res = {"circuit_ms_vs_qubits": {}, "fused_pass": {}, "per_gate_n30": {}}
     peak, _ = load_peaks()
     plan = [("qft", "c128", (16, 20, 24, 28, 30)), ("qft", "c64", (20, 26, 30)),
-            ("tfxy", "c128", (16, 20, 24, 28))]
+            ("tfxy", "c128", (16, 20, 24, 28, 30)), ("tfxy", "c64", (20, 28))]
+    fma = {"c128": qc.qc.fma_peak(True), "c64": qc.qc.fma_peak(False)}
+    res["fma_peak_TFLOPs"] = {"fp64": fma["c128"], "fp32": fma["c64"]}
     for fam, prec, ns in plan:
         key = f"{fam}_{prec}" + ("_S10" if fam == "tfxy" else "")
         res["circuit_ms_vs_qubits"][key] = {}
@@ -370,6 +408,9 @@ def sweep(args, local_rank):
             sb = (16 if prec == "c128" else 8) << n
             entry = {"ms": round(t, 4), "gates": len(ops), "passes": inf["last_passes"],
                      "jit": inf["last_jit"]}
+            alg = circuit_flops(ops, n) / (t / 1e3) / 1e12
+            entry["alg_TFLOPs"] = round(alg, 2)
+            entry["alg_flops_frac_of_fma_peak"] = round(alg / fma[prec], 4)
             if n >= 28:
                 gbps = 2 * sb * inf["last_passes"] / (t / 1e3) / 1e9
                 entry["fused_pass_GBps"] = round(gbps, 1)
@@ -389,8 +430,10 @@ def sweep(args, local_rank):
             t = _time_runs(s, qc.encode_ops(ops), warm=4 if fam == "qft" else 2, reps=2)
             inf = s.info()
             gbps = 2 * (16 << 33) * inf["last_passes"] / (t / 1e3) / 1e9
+            alg = circuit_flops(ops, 33) / (t / 1e3) / 1e12
             res["north_star_n33_c128"][f"{fam}33" + ("_S10" if fam == "tfxy" else "")] = {
                 "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
+                "alg_TFLOPs": round(alg, 2), "alg_flops_frac_of_fp64_peak": round(alg / fma["c128"], 4),
                 "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
             s.close()
             torch.cuda.empty_cache()

@@ -56,6 +56,12 @@ qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* o
  * updated.  Used to time NVLink exchanges in isolation. */
 qc_status qc_debug_exchange(qc_state* s, int g, int l);
 
+/* Measurement utility (needs a GPU): the FMA throughput of the current device
+ * in TFLOP/s (2 flops per FMA), FP64 (dbl != 0) or FP32, from a kernel of 8
+ * independent FMA chains per thread (best of 3 timed launches).  bench.py
+ * uses it as the ALU roofline peak of the fused pass. */
+qc_status qc_debug_fma_peak(int dbl, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

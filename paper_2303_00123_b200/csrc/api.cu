@@ -876,3 +876,10 @@ extern "C" qc_status qc_debug_exchange(qc_state* s, int g, int l) {
   }
   return QC_OK;
 }
+
+extern "C" qc_status qc_debug_fma_peak(int dbl, double* tflops) {
+  if (!tflops) return fail(QC_ERR_INVALID_ARG, "tflops is NULL");
+  const int r = fma_peak(dbl != 0, tflops);
+  if (r) return fail(QC_ERR_CUDA, "fma peak kernel: %s", cudaGetErrorString((cudaError_t)r));
+  return QC_OK;
+}

@@ -179,3 +179,55 @@ int launch_norm2(const void* state, int n, bool dbl, double* d_partial, int nblo
 }
 
 }  // namespace qc
+
+// ---------------------------------------------------------------- FMA peak
+// Measurement utility (qc_debug_fma_peak): 8 independent FMA chains per
+// thread, so the FP64 / FP32 pipe -- not latency -- bounds the loop.
+namespace qc {
+template <typename T>
+__global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
+  T x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const T s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == (T)-1.2345) out[0] = s;  // keep the chains live
+}
+
+int fma_peak(bool dbl, double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  void* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, 64);
+  if (e != cudaSuccess) return (int)e;
+  const int blocks = sms * 4, threads = 512, iters = dbl ? 4096 : 16384;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    if (dbl)
+      fma_peak_kernel<double><<<blocks, threads>>>((double*)out, iters, 0.999999, 1e-7);
+    else
+      fma_peak_kernel<float><<<blocks, threads>>>((float*)out, iters, 0.999f, 1e-3f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  const double flops = 2.0 * 64.0 * (double)iters * threads * blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return (int)e;
+}
+}  // namespace qc

@@ -136,5 +136,6 @@ int launch_gather(const void* state, void* dst, int n, bool dbl, const int* layo
 int launch_norm2(const void* state, int n, bool dbl, double* d_partial, int nblocks,
                  void* stream);
 int sm_count();
+int fma_peak(bool dbl, double* tflops);  // measurement utility (qc_debug_fma_peak)
 
 }  // namespace qc

@@ -69,7 +69,8 @@ class qc_plan_stats(ctypes.Structure):
                 ("restore_passes", ctypes.c_int64)]
 
 
-DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange"]
+DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange",
+                 "qc_debug_fma_peak"]
 
 _lib = None
 
@@ -113,6 +114,8 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_dist_schedule.restype = ctypes.c_int
     L.qc_debug_exchange.argtypes = [vp, i32, i32]
     L.qc_debug_exchange.restype = ctypes.c_int
+    L.qc_debug_fma_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double)]
+    L.qc_debug_fma_peak.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
     L.qc_version.restype = ctypes.c_char_p
     for name in EXPORTS:
@@ -301,6 +304,15 @@ def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_f
     if rc != QC_OK:
         raise QCError(rc, eb.value.decode())
     return {f: getattr(st, f) for f, _ in qc_plan_stats._fields_}
+
+
+def fma_peak(dbl: bool = True) -> float:
+    """Measured FMA throughput of the current device, TFLOP/s (qc_debug.h)."""
+    v = ctypes.c_double(0.0)
+    rc = lib().qc_debug_fma_peak(int(dbl), ctypes.byref(v))
+    if rc != QC_OK:
+        raise QCError(rc, lib().qc_last_error().decode())
+    return v.value
 
 
 def nccl_unique_id() -> bytes:

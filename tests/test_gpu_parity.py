@@ -377,3 +377,11 @@ def test_remap_permutation_circuit_bit_exact(qcmod):
     for prec in ("c128", "c64"):
         got, info = gpu_run(qcmod, n, prec, ops, tile_bits=8, jit=2)
         assert np.array_equal(got.astype(np.complex128), ref_run(n, prec, ops))
+
+
+def test_fma_peak_measurement(qcmod):
+    """The ALU roofline denominator bench.py reports (qc_debug_fma_peak)."""
+    p64 = qcmod.qc.fma_peak(True)
+    p32 = qcmod.qc.fma_peak(False)
+    assert 10.0 < p64 < 200.0, p64
+    assert p32 > p64, (p32, p64)
