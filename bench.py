@@ -243,7 +243,7 @@ def run_ours(args, rank, world, local_rank):
     avg_launch_ms = ms_per_step / max(launches_per_step, 1)
     achieved = 2 * state_bytes / (avg_launch_ms / 1e3) / 1e9
     fma_peak = qc.qc.fma_peak(prec == "c128")
-    flops = circuit_flops(ops, n)
+    flops = info["last_flops_per_amp"] * float(1 << n)
     alu_achieved = flops / max(launches_per_step, 1) / (avg_launch_ms / 1e3) / 1e12
     traffic, traffic_src = load_traffic(args.config)
     hbm_view = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -253,8 +253,10 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": f"measured {'FP64' if prec == 'c128' else 'FP32'} FMA peak (qc_debug_fma_peak, "
                                "8 independent FMA chains/thread, this GPU, this run)",
                 "flops_per_launch": flops / max(launches_per_step, 1),
-                "flops_note": "algorithmic = unfused per-gate flops/amp (dense 1q 14, dense 2q 30, diagonal "
-                              "6 per touched amp, permutations 0) x 2^n, / fused launches per step"}
+                "flops_note": "algorithmic flops of the fused plan's ops (qc_info.last_flops_per_amp: complex "
+                              "arithmetic, general cmul 6 / cmac 8 flops, unit coefficients free, x fraction of "
+                              "amplitudes touched) x 2^n, / fused launches per step",
+                "unfused_gate_flops_per_step": circuit_flops(ops, n)}
     main_view = alu_view if fam == "tfxy" else hbm_view
     out = {
         "metric": METRIC, "value": value, "unit": "circuit/s", "n_gpus": world,
@@ -408,9 +410,9 @@ def sweep(args, local_rank):
             sb = (16 if prec == "c128" else 8) << n
             entry = {"ms": round(t, 4), "gates": len(ops), "passes": inf["last_passes"],
                      "jit": inf["last_jit"]}
-            alg = circuit_flops(ops, n) / (t / 1e3) / 1e12
-            entry["alg_TFLOPs"] = round(alg, 2)
-            entry["alg_flops_frac_of_fma_peak"] = round(alg / fma[prec], 4)
+            alg = inf["last_flops_per_amp"] * float(1 << n) / (t / 1e3) / 1e12
+            entry["fused_alg_TFLOPs"] = round(alg, 2)
+            entry["fused_alg_flops_frac_of_fma_peak"] = round(alg / fma[prec], 4)
             if n >= 28:
                 gbps = 2 * sb * inf["last_passes"] / (t / 1e3) / 1e9
                 entry["fused_pass_GBps"] = round(gbps, 1)
@@ -430,10 +432,10 @@ def sweep(args, local_rank):
             t = _time_runs(s, qc.encode_ops(ops), warm=4 if fam == "qft" else 2, reps=2)
             inf = s.info()
             gbps = 2 * (16 << 33) * inf["last_passes"] / (t / 1e3) / 1e9
-            alg = circuit_flops(ops, 33) / (t / 1e3) / 1e12
+            alg = inf["last_flops_per_amp"] * float(1 << 33) / (t / 1e3) / 1e12
             res["north_star_n33_c128"][f"{fam}33" + ("_S10" if fam == "tfxy" else "")] = {
                 "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
-                "alg_TFLOPs": round(alg, 2), "alg_flops_frac_of_fp64_peak": round(alg / fma["c128"], 4),
+                "fused_alg_TFLOPs": round(alg, 2), "fused_alg_flops_frac_of_fp64_peak": round(alg / fma["c128"], 4),
                 "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
             s.close()
             torch.cuda.empty_cache()

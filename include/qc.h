@@ -133,6 +133,9 @@ typedef struct qc_info {
     int32_t n_local;          /* qubits per shard (n - log2 world)               */
     int32_t sharding;         /* 0 single GPU, 1 loopback (all shards here), 2 NCCL */
     int64_t last_exchanges;   /* qubit-swap exchanges in the last run            */
+    double last_flops_per_amp; /* fused runs: algorithmic flops per amplitude of the
+                                  plan's fused ops (complex arithmetic counted;
+                                  the ALU roofline numerator, qc_debug.h)      */
 } qc_info;
 
 /* ---------------------------------------------------------------- lifetime */

@@ -29,6 +29,7 @@ typedef struct qc_plan_stats {
     int32_t jit_compiled; /* passes compiled by NVRTC (compile_jit != 0)    */
     int64_t remap_swaps;  /* row-bit <-> tile-bit remap swaps (remap != 0)  */
     int64_t restore_passes; /* swap-only passes restoring the input layout  */
+    double flops_per_amp; /* algorithmic flops per amplitude of the fused ops */
 } qc_plan_stats;
 
 /* tile_bits / row_bits 0 = default; remap as QC_OPT_REMAP.  errbuf (may be

@@ -177,6 +177,7 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap);
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
   e->perm = fp.perm;
+  e->flops_per_amp = plan_flops_per_amp(fp);
   const bool g4 = s->tma_mode == 0 && make_row_tmap(tmap_base ? tmap_base : s->d, tmap_bits ? tmap_bits : n_plan, rb,
                                                      s->dbl, &e->tmap);
   for (auto& p : fp.passes) {
@@ -327,6 +328,7 @@ qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   s->last_k = e->tile_bits;
   s->last_blocks = e->fused_gates;
   s->last_jit = e->jit_state == 1 ? 1 : 0;
+  s->last_flops_per_amp = e->flops_per_amp;
   return QC_OK;
 }
 
@@ -765,6 +767,7 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
   out->n_local = s->dist ? s->n_loc : s->n;
   out->sharding = s->dist;
   out->last_exchanges = s->last_exchanges;
+  out->last_flops_per_amp = s->last_flops_per_amp;
   return QC_OK;
 }
 
@@ -810,6 +813,7 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   FusedPlan fp = plan_fused(n, k, rb, blocks, remap != 0);
   if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
   out->remap_swaps = fp.remap_swaps;
+  out->flops_per_amp = plan_flops_per_amp(fp);
   out->restore_passes = fp.restore_passes;
   // mirror build_fused_entry's layout choice (make_row_tmap's gather4 limits)
   const bool g4 = ((uint64_t)(dbl ? 16 : 8) << rb) <= 1024 && n - rb <= 31 && n - rb >= 2;

@@ -780,6 +780,48 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
   return plan;
 }
 
+// Algorithmic flops per state amplitude of a fused plan: what the fused ops
+// must compute, counted as complex arithmetic (a general complex multiply 6
+// flops, multiply-accumulate 8; multiplying by +-1 / +-i free, accumulating
+// it 2), times the fraction of amplitudes each op touches (predicates halve
+// it per bit, identity rows and the d0 = 1 half of a diagonal are skipped).
+// The ALU roofline of bench.py divides this work by the pass time.
+double plan_flops_per_amp(const FusedPlan& plan) {
+  auto unit = [](cd z) {
+    return (std::abs(z.imag()) == 0.0 && std::abs(z.real()) == 1.0) ||
+           (z.real() == 0.0 && std::abs(z.imag()) == 1.0);
+  };
+  double total = 0;
+  for (const auto& pp : plan.passes)
+    for (const auto& o : pp.ops) {
+      if (o.folded) continue;
+      const FHdr& h = o.h;
+      const double pred = std::ldexp(1.0, -(popc(h.smask) + popc(h.lmask) + popc(h.omask)));
+      if (h.kind == F_M1 || h.kind == F_M2) {
+        const int dim = h.kind == F_M1 ? 2 : 4;
+        double f = 0;
+        for (int r = 0; r < dim; ++r) {
+          double fr = 0;
+          bool first = true, ident = true;
+          for (int c = 0; c < dim; ++c) {
+            const cd z = o.dense[r * dim + c];
+            if (r == c ? !(z.real() == 1.0 && z.imag() == 0.0) : !is0(z)) ident = false;
+            if (is0(z)) continue;
+            fr += first ? (unit(z) ? 0 : 6) : (unit(z) ? 2 : 8);
+            first = false;
+          }
+          if (!ident) f += fr;
+        }
+        total += f / dim * pred;
+      } else if (h.kind == F_DSCALE) {
+        total += 6.0 * ((h.flags & 1) ? 0.5 : 1.0) * pred;
+      } else {  // F_PRUN: one complex factor per amplitude (the d0 = 1 half skipped)
+        total += 6.0 * ((h.flags & 1) || !o.sterms.empty() ? 1.0 : 0.5) * pred;
+      }
+    }
+  return total;
+}
+
 namespace {
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 

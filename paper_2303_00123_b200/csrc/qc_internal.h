@@ -91,6 +91,8 @@ struct FusedPlan {
 // Planner (plan.cpp).  k = tile bits (<= n), returns passes covering all gates.
 // remap: passes may end with swaps of row bits and tile bits (plan.perm).
 FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates, bool remap = false);
+// Algorithmic flops per amplitude of the fused plan (ALU roofline numerator).
+double plan_flops_per_amp(const FusedPlan& plan);
 // Pack the plan into one device blob for precision T (fills desc.blob_*).
 std::vector<uint8_t> pack_plan(FusedPlan& plan, bool dbl);
 

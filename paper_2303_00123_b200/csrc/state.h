@@ -30,6 +30,7 @@ struct PlanEntry {
   int ctas = 0;
   int tile_bits = 0;
   std::vector<int> perm;             // remap: data of physical bit p ends at perm[p]
+  double flops_per_amp = 0;          // plan_flops_per_amp
   ~PlanEntry() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -99,6 +100,7 @@ struct qc_state {
   int last_graph = 0, last_k = 0;
   int64_t last_blocks = 0;
   int last_jit = 0;
+  double last_flops_per_amp = 0;
   // plan cache
   std::unordered_map<uint64_t, std::unique_ptr<qc::PlanEntry>> plans;
   cudaStream_t cap_stream = nullptr;

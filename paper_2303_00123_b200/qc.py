@@ -57,7 +57,8 @@ class qc_info(ctypes.Structure):
                 ("last_graph", ctypes.c_int32), ("tile_bits", ctypes.c_int32),
                 ("last_blocks", ctypes.c_int64), ("last_jit", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("n_local", ctypes.c_int32),
-                ("sharding", ctypes.c_int32), ("last_exchanges", ctypes.c_int64)]
+                ("sharding", ctypes.c_int32), ("last_exchanges", ctypes.c_int64),
+                ("last_flops_per_amp", ctypes.c_double)]
 
 
 class qc_plan_stats(ctypes.Structure):
@@ -66,7 +67,7 @@ class qc_plan_stats(ctypes.Structure):
                 ("fused_ops", ctypes.c_int64), ("phase_runs", ctypes.c_int64),
                 ("blob_bytes", ctypes.c_int64), ("tile_bits", ctypes.c_int32),
                 ("jit_compiled", ctypes.c_int32), ("remap_swaps", ctypes.c_int64),
-                ("restore_passes", ctypes.c_int64)]
+                ("restore_passes", ctypes.c_int64), ("flops_per_amp", ctypes.c_double)]
 
 
 DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange",
@@ -282,7 +283,7 @@ class State:
                 "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits,
                 "last_blocks": i.last_blocks, "last_jit": bool(i.last_jit), "world": i.world,
                 "rank": i.rank, "n_local": i.n_local, "sharding": i.sharding,
-                "last_exchanges": i.last_exchanges}
+                "last_exchanges": i.last_exchanges, "last_flops_per_amp": i.last_flops_per_amp}
 
     @property
     def stream(self) -> int:

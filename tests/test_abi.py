@@ -45,7 +45,26 @@ def test_gate_struct_layout_matches_header():
     assert qc.GATE_DTYPE.itemsize == 288
     assert qc.GATE_DTYPE.fields["theta"][1] == 24
     assert qc.GATE_DTYPE.fields["m"][1] == 32
-    assert ctypes.sizeof(qc.qc_info) == 368  # natural alignment of the qc_info fields in qc.h
+    # struct sizes / offsets as the C compiler lays out include/qc.h and qc_debug.h
+    import subprocess, tempfile
+    src = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "qc_debug.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu\n", sizeof(qc_gate), sizeof(qc_info), offsetof(qc_info, last_flops_per_amp),
+         sizeof(qc_plan_stats), offsetof(qc_plan_stats, flops_per_amp));
+  return 0;
+}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "t.c"), os.path.join(d, "t")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        sz = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert sz[0] == qc.GATE_DTYPE.itemsize
+    assert sz[1] == ctypes.sizeof(qc.qc_info) and sz[2] == qc.qc_info.last_flops_per_amp.offset
+    assert sz[3] == ctypes.sizeof(qc.qc_plan_stats) and sz[4] == qc.qc_plan_stats.flops_per_amp.offset
 
 
 def test_op_codes_match_header():
