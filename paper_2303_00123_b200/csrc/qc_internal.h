@@ -114,6 +114,7 @@ struct JitKernel {
   void* f = nullptr;  // CUfunction
   size_t smem = 0;
   int nbuf = 3;
+  int threads = kFusedThreads;  // compute warps * 32 + the TMA producer warp
 };
 bool jit_available(std::string* why);
 bool jit_build(const FusedPlan& plan, bool dbl, std::vector<JitKernel>& out, std::string& err);
