@@ -314,6 +314,17 @@ __device__ __forceinline__ void qc_swap(C& a, C& b) {
   b = t;
 }
 
+// Lane-dependent swap as selects (no divergent branch: both paths would need
+// their own copies of the 16 registers and a reconvergence point).
+template <typename C>
+__device__ __forceinline__ void qc_cswap(bool p, C& a, C& b) {
+  const C x = a, y = b;
+  a.x = p ? y.x : x.x;
+  a.y = p ? y.y : x.y;
+  b.x = p ? x.x : y.x;
+  b.y = p ? x.y : y.y;
+}
+
 template <int B, typename C>
 __device__ __forceinline__ void qc_prun_slot(C (&v)[kSlots], const C w0, const C w1, bool any0) {
 #pragma unroll
