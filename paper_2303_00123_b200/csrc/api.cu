@@ -153,7 +153,7 @@ void plan_geometry(const qc_state* s, int n_plan, int* k_out, int* rb_out, int* 
   int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
   if (s->dbl && k > 12) k = 12;  // two 2^k tiles (one per compute group) must fit in smem
   if (k > n_plan) k = n_plan;
-  int rb = s->row_bits ? s->row_bits : 6;  // 1 KiB (c128) / 512 B rows: gather4 at ~full HBM
+  int rb = s->row_bits ? s->row_bits : (s->dbl ? 6 : 7);  // 1 KiB rows: half the TMA requests of 512 B rows
   if (rb > k - 2) rb = k - 2;
   if (rb < 1) rb = 1;
   *k_out = k;
@@ -791,7 +791,7 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   int k = tile_bits ? tile_bits : (dbl ? 12 : 13);
   if (dbl && k > 12) k = 12;
   if (k > n) k = n;
-  int rb = row_bits ? row_bits : 6;
+  int rb = row_bits ? row_bits : (dbl ? 6 : 7);
   if (rb > k - 2) rb = k - 2;
   if (rb < 1) rb = 1;
   int lay[64];
