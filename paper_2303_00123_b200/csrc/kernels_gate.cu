@@ -29,49 +29,62 @@ __device__ __forceinline__ uint64_t insert0(uint64_t x, int p) {
   return ((x >> p) << (p + 1)) | lo;
 }
 
+// One work item (pair / quad / amplitude) of a gate: load phase then store
+// phase, so a thread can issue the loads of several items before any store.
 template <typename T, int KIND>
-__global__ void __launch_bounds__(256) gate_kernel(typename CT<T>::type* __restrict__ s,
-                                                   const GateArgs<T> a) {
+struct Item {
   using C = typename CT<T>::type;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.count; j += stride) {
+  uint64_t id[4];
+  C v[4];
+  __device__ __forceinline__ void load(const C* __restrict__ s, const GateArgs<T>& a, uint64_t j) {
     uint64_t x = j;
 #pragma unroll 4
     for (int i = 0; i < 4; ++i)
       if (i < a.nins) x = insert0(x, a.ins[i]);
     x |= a.setmask;
-    if (KIND == (int)GK::DENSE1) {
-      const uint64_t ia = x, ib = x | (1ull << a.t0);
-      const C u = s[ia], v = s[ib];
-      C o0, o1;
-      o0.x = a.m[0] * u.x - a.m[1] * u.y + a.m[2] * v.x - a.m[3] * v.y;
-      o0.y = a.m[0] * u.y + a.m[1] * u.x + a.m[2] * v.y + a.m[3] * v.x;
-      o1.x = a.m[4] * u.x - a.m[5] * u.y + a.m[6] * v.x - a.m[7] * v.y;
-      o1.y = a.m[4] * u.y + a.m[5] * u.x + a.m[6] * v.y + a.m[7] * v.x;
-      s[ia] = o0;
-      s[ib] = o1;
-    } else if (KIND == (int)GK::PERM1) {
-      const uint64_t ia = x, ib = x | (1ull << a.t0);
-      const C u = s[ia], v = s[ib];
-      s[ia] = v;
-      s[ib] = u;
+    if (KIND == (int)GK::DENSE1 || KIND == (int)GK::PERM1) {
+      id[0] = x;
+      id[1] = x | (1ull << a.t0);
+      v[0] = s[id[0]];
+      v[1] = s[id[1]];
     } else if (KIND == (int)GK::DIAG1) {
-      // d0 == 1: x already has the target bit set (inserted + setmask).
-      const int bit = (int)((x >> a.t0) & 1ull);
-      const T dr = a.m[2 * bit], di = a.m[2 * bit + 1];
-      const C u = s[x];
-      C o;
-      o.x = dr * u.x - di * u.y;
-      o.y = dr * u.y + di * u.x;
-      s[x] = o;
+      id[0] = x;
+      v[0] = s[x];
     } else if (KIND == (int)GK::DENSE2) {
-      uint64_t id[4];
-      C v[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         id[r] = x | ((uint64_t)((r >> 1) & 1) << a.t0) | ((uint64_t)(r & 1) << a.t1);
         v[r] = s[id[r]];
       }
+    } else {  // SWAP2
+      id[0] = x | (1ull << a.t0);
+      id[1] = x | (1ull << a.t1);
+      v[0] = s[id[0]];
+      v[1] = s[id[1]];
+    }
+  }
+  __device__ __forceinline__ void store(C* __restrict__ s, const GateArgs<T>& a) const {
+    if (KIND == (int)GK::DENSE1) {
+      const C u = v[0], w = v[1];
+      C o0, o1;
+      o0.x = a.m[0] * u.x - a.m[1] * u.y + a.m[2] * w.x - a.m[3] * w.y;
+      o0.y = a.m[0] * u.y + a.m[1] * u.x + a.m[2] * w.y + a.m[3] * w.x;
+      o1.x = a.m[4] * u.x - a.m[5] * u.y + a.m[6] * w.x - a.m[7] * w.y;
+      o1.y = a.m[4] * u.y + a.m[5] * u.x + a.m[6] * w.y + a.m[7] * w.x;
+      s[id[0]] = o0;
+      s[id[1]] = o1;
+    } else if (KIND == (int)GK::PERM1 || KIND == (int)GK::SWAP2) {  // pure moves (bit-exact)
+      s[id[0]] = v[1];
+      s[id[1]] = v[0];
+    } else if (KIND == (int)GK::DIAG1) {
+      // d0 == 1: x already has the target bit set (inserted + setmask).
+      const int bit = (int)((id[0] >> a.t0) & 1ull);
+      const T dr = a.m[2 * bit], di = a.m[2 * bit + 1];
+      C o;
+      o.x = dr * v[0].x - di * v[0].y;
+      o.y = dr * v[0].y + di * v[0].x;
+      s[id[0]] = o;
+    } else {  // DENSE2
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         T ore = 0, oim = 0;
@@ -86,12 +99,30 @@ __global__ void __launch_bounds__(256) gate_kernel(typename CT<T>::type* __restr
         o.y = oim;
         s[id[r]] = o;
       }
-    } else {  // SWAP2
-      const uint64_t ib = x | (1ull << a.t0), ic = x | (1ull << a.t1);
-      const C u = s[ib], v = s[ic];
-      s[ib] = v;
-      s[ic] = u;
     }
+  }
+};
+
+// Grid-stride loop, U items per thread per iteration (items j + u*stride:
+// consecutive lanes stay on consecutive indices), all U items' loads issued
+// before their stores -- U x the bytes in flight per thread.
+template <typename T, int KIND>
+__global__ void __launch_bounds__(256) gate_kernel(typename CT<T>::type* __restrict__ s,
+                                                   const GateArgs<T> a) {
+  constexpr int U = KIND == (int)GK::DENSE2 ? 2 : 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; j + (U - 1) * stride < a.count; j += U * stride) {
+    Item<T, KIND> it[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) it[u].load(s, a, j + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) it[u].store(s, a);
+  }
+  for (; j < a.count; j += stride) {  // tail
+    Item<T, KIND> it;
+    it.load(s, a, j);
+    it.store(s, a);
   }
 }
 
