@@ -258,8 +258,10 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       return QC_OK;
     }
     const uint64_t local_mask = (1ull << nl) - 1;
+    // remap on: the plan ends in the layout it started from (restore passes),
+    // so the exchange slot keeps the qubit the preceding SWAP2 put there
     const qc_status r = build_fused_entry(s, seg, nl, local_mask, st.seg.get(), s->d,
-                                          s->dist == 1 ? n : nl);
+                                          s->dist == 1 ? n : nl, s->remap != 0);
     if (r != QC_OK) return r;
     P->passes += (int64_t)st.seg->passes.size();
     P->steps.push_back(std::move(st));
