@@ -235,6 +235,28 @@ qc_status qc_state_norm2(qc_state* s, double* out);
 qc_status qc_set_option(qc_state* s, qc_option opt, int64_t value);
 qc_status qc_get_info(const qc_state* s, qc_info* out);
 
+/* ------------------------------------------------------------ openQASM 2.0
+ * The paper's I/O statement (P:6: "provides I/O through openQASM"); grammar
+ * per SPEC S:442-495: header `OPENQASM 2.0;`, the literal
+ * `include "qelib1.inc";`, exactly one `qreg`, gate statements h x y z,
+ * p|u1, rx ry rz, cx|CX, cz, cp|cu1, swap, ccx with constant angle
+ * expressions (+ - * /, unary minus, parentheses, numbers, pi), `//`
+ * comments.  creg / measure / reset / barrier / if / gate definitions /
+ * a second qreg are rejected.  Host-only (no device work, no state).
+ *
+ * qc_qasm_parse: text (NUL-terminated, borrowed) -> *n_qubits and the gate
+ *   list in program order; writes min(cap, count) gates to `ops` (may be
+ *   NULL to query) and always sets *n_ops = count.  Errors: QC_ERR_INVALID_ARG
+ *   with "line:col: what" in qc_last_error().
+ * qc_qasm_emit: gate list -> text ("OPENQASM 2.0;\ninclude \"qelib1.inc\";\n
+ *   qreg q[n];\n" + one statement per gate, angles with 17 significant
+ *   digits; P -> u1, CP -> cu1, CNOT -> cx).  Writes at most cap-1 bytes + NUL
+ *   to buf (may be NULL to query) and always sets *len = full length.
+ *   Errors: QC_ERR_INVALID_ARG (invalid gate), QC_ERR_UNSUPPORTED (U1 / CU1 /
+ *   U2 generic matrices or |0> controls: no qelib1 name). */
+qc_status qc_qasm_parse(const char* text, int* n_qubits, qc_gate* ops, size_t cap, size_t* n_ops);
+qc_status qc_qasm_emit(int n, const qc_gate* ops, size_t n_ops, char* buf, size_t cap, size_t* len);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char* qc_last_error(void);
 

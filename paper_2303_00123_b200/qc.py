@@ -39,7 +39,8 @@ EXPORTS = ["qc_state_create", "qc_state_create_ex", "qc_state_wrap", "qc_state_d
            "qc_state_create_dist", "qc_state_create_loopback", "qc_nccl_unique_id",
            "qc_state_init_basis", "qc_state_init_random", "qc_apply_gate", "qc_run_circuit",
            "qc_state_read", "qc_state_write", "qc_state_canonicalize", "qc_state_sync",
-           "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_last_error", "qc_version"]
+           "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_qasm_parse", "qc_qasm_emit",
+           "qc_last_error", "qc_version"]
 
 
 class QCError(RuntimeError):
@@ -119,6 +120,10 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_fma_peak.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
     L.qc_version.restype = ctypes.c_char_p
+    L.qc_qasm_parse.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), vp, sz, ctypes.POINTER(ctypes.c_size_t)]
+    L.qc_qasm_parse.restype = ctypes.c_int
+    L.qc_qasm_emit.argtypes = [i32, vp, sz, ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_size_t)]
+    L.qc_qasm_emit.restype = ctypes.c_int
     for name in EXPORTS:
         f = getattr(L, name)
         if name not in ("qc_state_create", "qc_state_destroy", "qc_last_error", "qc_version"):
@@ -154,6 +159,30 @@ def encode_ops(ops: Iterable) -> np.ndarray:
             flat[1:2 * m.size:2] = m.imag
             arr[i]["m"] = flat
     return arr
+
+
+def qasm_parse(text: str):
+    """openQASM 2.0 text -> (n_qubits, qc_gate array) via qc_qasm_parse."""
+    b = text.encode()
+    n = ctypes.c_int(0)
+    cnt = ctypes.c_size_t(0)
+    _check(lib().qc_qasm_parse(b, ctypes.byref(n), None, 0, ctypes.byref(cnt)))
+    arr = np.zeros(cnt.value, dtype=GATE_DTYPE)
+    _check(lib().qc_qasm_parse(b, ctypes.byref(n), arr.ctypes.data if cnt.value else None, cnt.value,
+                               ctypes.byref(cnt)))
+    return n.value, arr
+
+
+def qasm_emit(n: int, ops) -> str:
+    """Gate list -> openQASM 2.0 text via qc_qasm_emit."""
+    arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
+    arr = np.ascontiguousarray(arr)
+    ln = ctypes.c_size_t(0)
+    p = arr.ctypes.data if len(arr) else None
+    _check(lib().qc_qasm_emit(n, p, len(arr), None, 0, ctypes.byref(ln)))
+    buf = ctypes.create_string_buffer(ln.value + 1)
+    _check(lib().qc_qasm_emit(n, p, len(arr), buf, ln.value + 1, ctypes.byref(ln)))
+    return buf.value.decode()
 
 
 class State:

@@ -385,3 +385,25 @@ def test_fma_peak_measurement(qcmod):
     p32 = qcmod.qc.fma_peak(False)
     assert 10.0 < p64 < 200.0, p64
     assert p32 > p64, (p32, p64)
+
+
+def test_qasm_program_on_gpu(qcmod):
+    """A circuit read from openQASM 2.0 text (qc_qasm_parse) runs through the
+    fused engine and matches the oracle on the same parsed list."""
+    n = 14
+    txt = qcmod.qc.qasm_emit(n, qcgen.qft(n) + qcgen.tfxy(n, 2))
+    n2, arr = qcmod.qc.qasm_parse(txt)
+    assert n2 == n
+    names = {v: k for k, v in qcmod.qc.OPS.items()}
+    ops = []
+    for g in arr:
+        name = names[int(g["op"])]
+        k = qcgen.ARITY[name]
+        ops.append(Op(name, tuple(int(q) for q in g["qubits"][:k]),
+                      theta=float(g["theta"]) if name in qcgen.THETA_OPS else None))
+    for prec in ("c128", "c64"):
+        with qcmod.State(n, prec) as s:
+            s.init_random(qcgen.STATE_SEED)
+            s.run(arr)
+            got = s.read()
+        assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec]
