@@ -205,7 +205,7 @@ int fma_peak(bool dbl, double* tflops) {
   void* out = nullptr;
   cudaError_t e = cudaMalloc(&out, 64);
   if (e != cudaSuccess) return (int)e;
-  const int blocks = sms * 4, threads = 512, iters = dbl ? 128 : 512;
+  const int blocks = sms * 4, threads = 512, iters = dbl ? 1024 : 4096;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
