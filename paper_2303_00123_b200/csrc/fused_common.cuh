@@ -414,7 +414,9 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
       if (i < my_n) {
         const uint64_t base = qc_tile_base(pd, blockIdx.x + i * gridDim.x) | pd.addr_bits;
         if (lane == 0) {
-          buf_tile[b] = (uint32_t)i;  // full[b]'s pending phase now belongs to tile i
+          // full[b]'s pending phase now belongs to tile i (atomic: the tag is
+          // polled by the consumer groups -- an explicit flag, not a data race)
+          atomicExch(const_cast<uint32_t*>(&buf_tile[b]), (uint32_t)i);
           qc_mbar_arrive_expect_tx(&full[b], tile_bytes);
         }
         __syncwarp();
@@ -445,7 +447,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     body.prologue(tbase, par);
     if (kGroups > 1 && NBUF % kGroups) {
       // wait until the producer has claimed buffer b for this tile (see fused_types.h)
-      while (buf_tile[b] != (uint32_t)i) __nanosleep(64);
+      while (atomicOr(const_cast<uint32_t*>(&buf_tile[b]), 0u) != (uint32_t)i) __nanosleep(64);
     }
     qc_mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1ull));
     body.tile(bufs + (size_t)b * buf_amps, tbase, par);
