@@ -30,6 +30,8 @@ typedef struct qc_plan_stats {
     int64_t remap_swaps;  /* row-bit <-> tile-bit remap swaps (remap != 0)  */
     int64_t restore_passes; /* swap-only passes restoring the input layout  */
     double flops_per_amp; /* algorithmic flops per amplitude of the fused ops */
+    int64_t swz_substages;  /* sub-stages with >= 2 slot bits among the smem
+                               bank-group bits (lane-XOR select network)     */
 } qc_plan_stats;
 
 /* tile_bits / row_bits 0 = default; remap as QC_OPT_REMAP.  errbuf (may be

@@ -822,7 +822,13 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
     pp.desc.pshift = g4 ? 31 : rb;
   }
   out->passes = (int64_t)fp.passes.size();
+  const int LB = dbl ? 3 : 4;  // tile bits inside one 16-B / 8-B bank-group phase (jit.cu)
   for (auto& pp : fp.passes) {
+    for (auto& sd : pp.subs) {
+      int x = 0;
+      for (int j = 0; j < kSlotBits; ++j) x += sd.g[j] < LB;
+      out->swz_substages += x >= 2;
+    }
     out->substages += (int64_t)pp.subs.size();
     out->fused_ops += (int64_t)pp.ops.size();
     for (auto& o : pp.ops) out->phase_runs += o.h.kind == F_PRUN;

@@ -68,7 +68,8 @@ class qc_plan_stats(ctypes.Structure):
                 ("fused_ops", ctypes.c_int64), ("phase_runs", ctypes.c_int64),
                 ("blob_bytes", ctypes.c_int64), ("tile_bits", ctypes.c_int32),
                 ("jit_compiled", ctypes.c_int32), ("remap_swaps", ctypes.c_int64),
-                ("restore_passes", ctypes.c_int64), ("flops_per_amp", ctypes.c_double)]
+                ("restore_passes", ctypes.c_int64), ("flops_per_amp", ctypes.c_double),
+                ("swz_substages", ctypes.c_int64)]
 
 
 DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange",
