@@ -1,22 +1,34 @@
-"""bench.py -- QFT / TFXY circuit time on B200 through libqc (the C ABI).
+"""bench.py -- QFT / TFXY state-vector circuit time on B200 through libqc (the C ABI).
 
-Default workload = BASELINE.json configs[1]: TFXY 1D Trotter circuit, 20
-qubits, 10 Trotter steps, complex double, random initial state, 1 B200.
-A "step" is one qc_run_circuit of the whole circuit on the resident state.
+Default workload at N = 1: BASELINE.json configs[3] (C4), the largest
+single-GPU configuration -- TFXY 1D Trotter circuit (DESIGN R8),
+33 qubits, 10 Trotter steps, complex double, a 137 GB state resident in HBM,
+seeded random initial state.  A "step" is one qc_run_circuit of the whole
+circuit on the resident state (all SURVEY 8(a) rows: fused tile passes with
+SWAP relabels and row-bit remaps).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config tfxy20|qft10|qft30|qft30c64|tfxy33] [--no-sweep]
+                  [--config tfxy33|tfxy20|qft10|qft30|qft30c64|tfxy_shard|qft_shard]
+                  [--no-sweep] [--no-cpu]
 
-Under torchrun (N > 1) every rank runs its own replica of the workload
-("replicas only": the default workload does not shard), timing
-is max over ranks, value = N*K circuits / max time ("scaling": "weak").
+N > 1: one process per GPU (torchrun; `--gpus N` without WORLD_SIZE re-execs
+itself under torch.distributed.run).  The default N > 1 workload is the
+sharded weak-scaling grid of SURVEY 8(d): TFXY S=10 at n = 33 + log2 N
+(128 GiB per GPU), sharded by the top log2 N qubits with NCCL qubit-swap
+exchanges (`--config qft_shard`: BASELINE configs[4], QFT n = 33 + log2 N,
+= C5 at N = 8).
+
+value = whole-job throughput in amplitude-gate updates per second: gates of
+the circuit x 2^n amplitudes / circuit time (units all ranks processed / max
+time over ranks), reported in 1e9 ("Gamp-gate/s"); circuits/s and ms per
+circuit are in the line too.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -29,25 +41,38 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "QFT & TFXY circuit time vs qubits at 1-8 B200; per-gate HBM GB/s vs peak"
+UNIT = "Gamp-gate/s"
 
 CONFIGS = {
-    # name: (family, n, steps, precision, description)
-    "qft10": ("qft", 10, 0, "c128", "QFT on 10 qubits, complex double, random initial state"),
-    "tfxy20": ("tfxy", 20, 10, "c128", "TFXY 1D Trotter circuit, 20 qubits, 10 time steps, complex double, 1 B200"),
-    "qft30": ("qft", 30, 0, "c128", "QFT on 30 qubits, complex double, 1 B200"),
-    "qft30c64": ("qft", 30, 0, "c64", "QFT on 30 qubits, complex single, 1 B200"),
-    "tfxy33": ("tfxy", 33, 10, "c128", "TFXY Trotter circuit, 33 qubits complex double, 1 B200"),
-    # sharded (one process per GPU, NCCL qubit-swap exchanges): n = local + log2(N)
-    "qft_shard": ("qft", None, 0, "c128",
-                  "QFT complex double sharded over N B200 by the top log2(N) qubits (weak scaling)"),
+    # name: (family, n (None: 33 + log2 N), trotter steps, precision, description)
+    "qft10": ("qft", 10, 0, "c128", "C1: QFT on 10 qubits, complex double, random initial state"),
+    "tfxy20": ("tfxy", 20, 10, "c128", "C2: TFXY 1D Trotter circuit, 20 qubits, 10 time steps, complex double, "
+                                       "1 B200 (16 MiB state, L2-resident)"),
+    "qft30": ("qft", 30, 0, "c128", "C3: QFT on 30 qubits, complex double, 1 B200"),
+    "qft30c64": ("qft", 30, 0, "c64", "C3: QFT on 30 qubits, complex single, 1 B200"),
+    "tfxy33": ("tfxy", 33, 10, "c128", "C4: TFXY Trotter circuit, 33 qubits, 10 time steps, complex double "
+                                       "(137 GB state), 1 B200"),
+    # sharded (one process per GPU, qubit-swap exchanges): n = local + log2(N)
+    "tfxy_shard": ("tfxy", None, 10, "c128", "TFXY Trotter circuit S=10, complex double, n = 33 + log2(N) "
+                                             "sharded over N B200 by the top log2(N) qubits (weak scaling)"),
+    "qft_shard": ("qft", None, 0, "c128", "C5: QFT complex double, n = 33 + log2(N) sharded over N B200 by the "
+                                          "top log2(N) qubits (weak scaling; n=36 at N=8)"),
 }
 
 
-def build_ops(cfg, n=None):
+def default_config(world):
+    return "tfxy33" if world == 1 else "tfxy_shard"
+
+
+def build_ops(cfg, n):
     import qcgen
-    fam, n0, steps, prec, _ = CONFIGS[cfg]
-    n = n0 if n is None else n
+    fam, _, steps, _, _ = CONFIGS[cfg]
     return qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, steps)
+
+
+def gamp(ops, n, seconds):
+    """amplitude-gate updates per second, in 1e9."""
+    return len(ops) * float(1 << n) / seconds / 1e9
 
 
 # Algorithmic flops per amplitude of each unfused gate (SURVEY 8(d)): dense
@@ -63,7 +88,7 @@ def circuit_flops(ops, n):
 
 def load_traffic(cfg):
     """dram read+write bytes per launch of qc_pass from the committed ncu
-    --set full capture of this workload (profiles/ncu_traffic.json), or None."""
+    capture of this workload (profiles/ncu_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f).get(cfg)
@@ -75,8 +100,7 @@ def load_traffic(cfg):
 def derived_fma_peak(prec, device=0):
     """ALU roofline denominator derived from unit counts and clocks (DESIGN
     section 6): SMs x FMA lanes per SM per clock (FP64 64, FP32 128 on
-    sm_100) x 2 flops x the max SM clock (MEASURED_PEAKS.json sm_max_mhz).
-    qc_debug_fma_peak measures 92 % of it (bench sweep, fma_peak_TFLOPs)."""
+    sm_100) x 2 flops x the max SM clock (MEASURED_PEAKS.json sm_max_mhz)."""
     import torch
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     try:
@@ -98,6 +122,17 @@ def load_peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 # ------------------------------------------------------------------ clocks
@@ -151,54 +186,117 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU oracle
-def cpu_oracle_rate(cfg: str, budget_s: float = 15.0, n_override=None):
-    """Time the oracle (as it stands) on the host cores on a bounded prefix of
-    the same circuit; returns circuits/s extrapolated from the prefix."""
-    import oracle
-    import qcgen
-    fam, n, steps, prec, _ = CONFIGS[cfg]
-    n = n if n_override is None else n_override
-    ops = build_ops(cfg, n)
-    n_s = min(n, 24)  # largest size the host holds comfortably for a bounded sample
-    st = qcgen.random_state(n_s, precision=prec)
-    sample_ops = ops if n_s == n else [o for o in ops if max(o.qubits) < n_s]
-    done, t0 = 0, time.perf_counter()
-    psi = st
-    chunk = 8
-    while done < len(sample_ops) and time.perf_counter() - t0 < budget_s:
-        psi = oracle.run(n_s, psi, sample_ops[done:done + chunk])
-        done += min(chunk, len(sample_ops) - done)
-    el = time.perf_counter() - t0
-    per_gate = el / max(done, 1) * (2.0 ** (n - n_s))
-    rate = 1.0 / (per_gate * len(ops))
-    sample = (f"first {done} of {len(ops)} gates of the {cfg} circuit at n={n_s}"
-              + ("" if n_s == n else f", per-gate time scaled x2 per qubit to n={n} (P:112 law)")
-              + f", {el:.1f} s")
-    return rate, oracle.max_threads(), sample
+class OracleSampler:
+    """The oracle (as it stands) on a BOUNDED sample of the workload: the
+    first gates of the circuit whose qubits lie below n_s, applied to the
+    seeded random state of n_s qubits.  Per-gate time is extrapolated to the
+    workload's n by x2 per qubit (the paper's scaling law) and to the
+    whole circuit by its gate count -- labelled "extrapolated" when n_s < n."""
+
+    def __init__(self, cfg, n, n_sample=26, step_s=2.0):
+        os.environ.setdefault("OMP_PROC_BIND", "close")  # before libgomp initialises
+        import oracle
+        import qcgen
+        self.oracle = oracle
+        self.cfg, self.n = cfg, n
+        self.ops = build_ops(cfg, n)
+        self.n_s = min(n, n_sample)
+        self.sample_ops = [o for o in self.ops if max(o.qubits) < self.n_s]
+        prec = CONFIGS[cfg][3]
+        self.psi = qcgen.random_state(self.n_s, precision=prec)
+        self.pos = 0
+        self.per_gate = []
+        # calibrate: gates per step so one step takes ~step_s
+        self._apply(1)  # first call loads the library
+        t = self._apply(1)
+        self.g_step = max(1, min(len(self.sample_ops), int(step_s / max(t, 1e-6))))
+
+    def _apply(self, g):
+        ops = [self.sample_ops[(self.pos + i) % len(self.sample_ops)] for i in range(g)]
+        self.pos = (self.pos + g) % len(self.sample_ops)
+        t0 = time.perf_counter()
+        self.psi = self.oracle.run(self.n_s, self.psi, ops)
+        dt = time.perf_counter() - t0
+        self.per_gate.append(dt / g)
+        return dt / g
+
+    def step(self):
+        t0 = time.perf_counter()
+        self._apply(self.g_step)
+        return time.perf_counter() - t0
+
+    def circuit_seconds(self, last=None):
+        pg = self.per_gate[-last:] if last else self.per_gate
+        return statistics.median(pg) * (2.0 ** (self.n - self.n_s)) * len(self.ops)
+
+    def describe(self, steps, secs):
+        ext = self.n_s < self.n
+        return (f"{steps} steps x {self.g_step} gates of the {self.cfg} circuit (its gates on qubits < {self.n_s}) "
+                f"at n={self.n_s}, {secs:.1f} s of oracle time; median per-gate time"
+                + (f" x2 per qubit to n={self.n} (P:112 law; extrapolated)" if ext else "")
+                + f" x {len(self.ops)} gates; {self.oracle.max_threads()} OpenMP threads, "
+                f"OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')}, host CPU: {cpu_model()}")
+
+
+def cpu_baseline(cfg, n, budget_s=15.0):
+    smp = OracleSampler(cfg, n)
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < budget_s:
+        smp.step()
+        k += 1
+    secs = time.perf_counter() - t0
+    csec = smp.circuit_seconds()
+    ops = smp.ops
+    return {"value": gamp(ops, n, csec), "unit": UNIT, "cores": smp.oracle.max_threads(), "kind": "oracle",
+            "extrapolated": smp.n_s < n, "circuit_s": csec, "sample": smp.describe(k, secs)}
 
 
 # ----------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_state(args, n, prec, rank, world, local_rank):
     import torch
     import paper_2303_00123_b200 as qc
+    if world == 1:
+        return qc.State(n, prec, device=local_rank)
+    uid = [qc.qc.nccl_unique_id() if rank == 0 else None]
+    torch.distributed.broadcast_object_list(uid, src=0)
+    return qc.State.dist(n, prec, rank, world, uid[0])
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    fam, n, steps_c, prec, desc = CONFIGS[args.config]
-    ops = build_ops(args.config)
+    fam, n0, steps_c, prec, desc = CONFIGS[args.config]
+    p = world.bit_length() - 1
+    n = n0 if n0 is not None else args.local_qubits + p
+    if n0 is not None and world > 1:
+        raise SystemExit(f"--config {args.config} is a single-GPU workload; use tfxy_shard / qft_shard for N > 1")
+    ops = build_ops(args.config, n)
+    import paper_2303_00123_b200 as qc
     arr = qc.encode_ops(ops)
-    s = qc.State(n, prec, device=local_rank)
+    s = make_state(args, n, prec, rank, world, local_rank)
     stream = torch.cuda.ExternalStream(s.stream, device=dev)
     s.init_random(12345)
-    state_bytes = (16 if prec == "c128" else 8) << n
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-
-    def step():
-        s.run(arr)
+    ab = 16 if prec == "c128" else 8
+    n_loc = n - p
+    shard_bytes = ab << n_loc
+    small = shard_bytes < (1 << 30)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if small else None
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            step()
+            s.run(arr)
         torch.cuda.synchronize()
         info = s.info()
         launches_per_step = info["last_launches"]
@@ -211,94 +309,116 @@ def run_ours(args, rank, world, local_rank):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed iterations (not inside the events)
+            if flush is not None:
+                flush.zero_()  # L2 flush between timed iterations (outside the events)
             ev[i][0].record(stream)
-            step()
+            s.run(arr)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         clocks = clk.stop()
     per = [a.elapsed_time(b) for a, b in ev]  # ms
-    t_total = sum(per)
-    if world > 1:
-        t = torch.tensor([t_total], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_total = float(t.item())
+    t_total = _max_over_ranks(sum(per), world, dev)
     ms_per_step = t_total / args.steps
-    value = world * args.steps / (t_total / 1e3)
+    value = gamp(ops, n, ms_per_step / 1e3)
+
+    # NVLink: one exchange of the top rank bit with the top local bit, timed alone
+    ex = None
+    if world > 1:
+        torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(4):
+                s.exchange(n - 1, n_loc - 1)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        te = _max_over_ranks(e0.elapsed_time(e1) / 4, world, dev)
+        bytes_dir = shard_bytes // 2
+        ex = {"ms": te, "bytes_per_direction": bytes_dir, "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9,
+              "frac_of_900": bytes_dir / (te / 1e3) / 1e9 / 900.0, "backend": "nccl send/recv"}
 
     # ---- e2e: pinned host state in, circuit, full state out, every step
     # (states above 8 GiB share one pinned buffer for input and output: the
     # read-back of step i is the upload of step i+1 -- same bytes moved)
-    h_in = torch.empty(state_bytes, dtype=torch.uint8, pin_memory=True)
-    h_out = h_in if state_bytes > (8 << 30) else torch.empty(state_bytes, dtype=torch.uint8, pin_memory=True)
-    s.read_ptr(h_in.data_ptr(), 1 << n)  # a valid state to start from
-    e2e_steps = max(1, min(args.steps, 5 if state_bytes <= (8 << 30) else 2))
+    h_in = torch.empty(shard_bytes, dtype=torch.uint8, pin_memory=True)
+    h_out = h_in if shard_bytes > (8 << 30) else torch.empty(shard_bytes, dtype=torch.uint8, pin_memory=True)
+    first = rank << n_loc
+    if world > 1:
+        s.canonicalize()
+    s.read_ptr(h_in.data_ptr(), 1 << n_loc, first)  # a valid state to start from
+    e2e_steps = max(1, min(args.steps, 5 if small else 2))
     torch.cuda.synchronize()
     e_ev = []
-    for i in range(e2e_steps + 1):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        s.write_ptr(h_in.data_ptr(), 1 << n)
-        s.run(arr)
-        s.read_ptr(h_out.data_ptr(), 1 << n)
-        b.record(stream)
-        if i > 0:
-            e_ev.append((a, b))
-    torch.cuda.synchronize()
-    e_ms = sum(a.elapsed_time(b) for a, b in e_ev) / len(e_ev)
-    if world > 1:
-        t = torch.tensor([e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(t.item())
+    with torch.cuda.stream(stream):
+        for i in range(e2e_steps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s.write_ptr(h_in.data_ptr(), 1 << n_loc, first)
+            s.run(arr)
+            if world > 1:
+                s.canonicalize()
+            s.read_ptr(h_out.data_ptr(), 1 << n_loc, first)
+            b.record(stream)
+            if i > 0:
+                e_ev.append((a, b))
+        torch.cuda.synchronize()
+    e_ms = _max_over_ranks(sum(a.elapsed_time(b) for a, b in e_ev) / len(e_ev), world, dev)
+    del h_in, h_out
 
     peak, peak_kind = load_peaks()
     # dominant kernel = the fused pass (every launch of the step is one).
-    # HBM view: algorithmic bytes per launch = read + write of the state (2*Ns).
+    # HBM view: algorithmic bytes per launch = read + write of the shard (2*Ns).
     # ALU view: algorithmic flops of the fused plan's ops per launch, against
-    # the FP64 (c128) / FP32 (c64) FMA peak derived from unit counts and
-    # clocks.  TFXY is bound by the FP64 pipe (block-fused pair blocks, ~8 FP64
-    # instructions per amplitude each), QFT by HBM.
+    # the FP64 (c128) / FP32 (c64) FMA peak derived from unit counts and clocks.
     avg_launch_ms = ms_per_step / max(launches_per_step, 1)
-    achieved = 2 * state_bytes / (avg_launch_ms / 1e3) / 1e9
+    achieved = 2 * shard_bytes / (avg_launch_ms / 1e3) / 1e9
     fma_peak, fma_src = derived_fma_peak(prec, local_rank)
-    flops = info["last_flops_per_amp"] * float(1 << n)
-    alu_achieved = flops / max(launches_per_step, 1) / (avg_launch_ms / 1e3) / 1e12
-    traffic, traffic_src = load_traffic(args.config)
+    flops = info["last_flops_per_amp"] * float(1 << n_loc)
+    alu_achieved = flops / (avg_launch_ms / 1e3) / 1e12
+    traffic, traffic_src = load_traffic(args.config if world == 1 else f"{fam}{n_loc}")
     hbm_view = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "bytes_per_launch": 2 * state_bytes}
+                "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "bytes_per_launch": 2 * shard_bytes}
     alu_view = {"bound": "alu", "achieved": alu_achieved, "peak": fma_peak, "unit": "TFLOP/s",
-                "frac": alu_achieved / fma_peak,
-                "peak_source": fma_src,
-                "flops_per_launch": flops / max(launches_per_step, 1),
+                "frac": alu_achieved / fma_peak, "peak_source": fma_src, "flops_per_launch": flops,
                 "flops_note": "algorithmic flops of the fused plan's ops (qc_info.last_flops_per_amp: complex "
                               "arithmetic, general cmul 6 / cmac 8 flops, unit coefficients free, x fraction of "
-                              "amplitudes touched) x 2^n, / fused launches per step",
+                              "amplitudes touched) x 2^n_local (one pass)",
                 "unfused_gate_flops_per_step": circuit_flops(ops, n)}
-    main_view = alu_view if fam == "tfxy" else hbm_view
+    # binding roof: the larger fraction (ALU for block-fused TFXY, HBM for QFT)
+    main_view = alu_view if alu_view["frac"] > hbm_view["frac"] else hbm_view
     out = {
-        "metric": METRIC, "value": value, "unit": "circuit/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if prec == "c128" else "f32", "data": "synthetic",
-        "config": {"workload": desc, "circuit": fam, "qubits": n, "trotter_steps": steps_c or None,
-                   "gates": len(ops), "precision": prec, "state_bytes": state_bytes,
+        "circuits_per_s": 1e3 / ms_per_step,
+        "config": {"workload": desc, "circuit": fam, "qubits": n, "local_qubits": n_loc,
+                   "trotter_steps": steps_c or None, "gates": len(ops), "precision": prec,
+                   "state_bytes": ab << n, "shard_bytes": shard_bytes,
                    "initial_state": "splitmix64 seed 12345 (DESIGN input recipe)",
-                   "l2": "flushed (512 MiB write) between timed iterations",
-                   "parallelism": f"replicas x{world}", "fused_passes_per_step": passes,
+                   "l2": ("flushed (512 MiB write) between timed iterations" if small else
+                          f"inputs larger than L2: {shard_bytes / 1e9:.1f} GB per GPU >> 126 MB"),
+                   "parallelism": "single GPU" if world == 1 else f"sharded x{world} by the top {p} qubits (NCCL)",
+                   "fused_passes_per_step": passes, "exchanges_per_step": info.get("last_exchanges", 0),
                    "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"],
-                   "jit_specialised": info["last_jit"], "ops_after_block_fusion": info["last_blocks"]},
+                   "jit_specialised": info["last_jit"], "ops_after_block_fusion": info["last_blocks"],
+                   "value_definition": "gates x 2^n / circuit time (max over ranks), 1e9 units"},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {**main_view, "kernel": "qc_pass (NVRTC-specialised fused tile pass)",
                      "traffic": traffic, "traffic_source": traffic_src,
                      "avg_launch_ms": avg_launch_ms, "hbm_view": hbm_view, "alu_view": alu_view,
                      "note": "avg launch = timed step time / fused launches per step (every launch of "
-                             "the step is a fused pass, timed by CUDA events on the state's stream)"},
-        "e2e": {"value": world / (e_ms / 1e3), "unit": "circuit/s", "h2d_bytes_per_step": state_bytes,
-                "d2h_bytes_per_step": state_bytes, "ms_per_step": e_ms},
+                             "the step is a fused pass, timed by CUDA events on the state's stream)"
+                             + ("; the step also holds the exchanges" if world > 1 else "")},
+        "e2e": {"value": gamp(ops, n, e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": shard_bytes,
+                "d2h_bytes_per_step": shard_bytes, "ms_per_step": e_ms,
+                "path": "qc_state_write (pinned host) + qc_run_circuit + qc_state_read (pinned host), per rank"},
         "clocks": clocks,
     }
+    if ex is not None:
+        out["nvlink_exchange"] = ex
     s.close()
     return out
 
@@ -317,92 +437,6 @@ def _time_runs(s, arr, warm=4, reps=3):
         b.record(stream)
         torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
-
-
-def run_sharded(args, rank, world, local_rank):
-    """QFT on a state sharded over `world` GPUs (qc_state_create_dist, NCCL
-    send/recv exchanges); weak scaling: 2^local_qubits amplitudes per GPU."""
-    import torch
-    import paper_2303_00123_b200 as qc
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    p = world.bit_length() - 1
-    n = args.local_qubits + p
-    prec = "c128"
-    ops = build_ops(args.config, n)
-    arr = qc.encode_ops(ops)
-    if world > 1:
-        uid = [qc.qc.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(uid, src=0)
-        s = qc.State.dist(n, prec, rank, world, uid[0])
-    else:
-        s = qc.State(n, prec, device=local_rank)
-    stream = torch.cuda.ExternalStream(s.stream, device=dev)
-    s.init_random(12345)
-    ab = 16
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            s.run(arr)
-        torch.cuda.synchronize()
-        info = s.info()
-        if world > 1:
-            torch.distributed.barrier()
-        clk = ClockSampler(local_rank)
-        clk.start()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            s.run(arr)
-        b.record(stream)
-        torch.cuda.synchronize()
-        clocks = clk.stop()
-        t = a.elapsed_time(b)
-        ex = None
-        if world > 1:  # NVLink: one exchange of the top rank bit with the top local bit, timed alone
-            torch.distributed.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 4
-            e0.record(stream)
-            for _ in range(reps):
-                s.exchange(n - 1, n - p - 1)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            te = e0.elapsed_time(e1) / reps
-            bytes_dir = (ab << (n - p)) // 2
-            ex = {"ms": te, "bytes_per_direction": bytes_dir, "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9}
-    tt = torch.tensor([t], device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        if ex is not None:
-            te_t = torch.tensor([ex["ms"]], device=dev)
-            torch.distributed.all_reduce(te_t, op=torch.distributed.ReduceOp.MAX)
-            ex["ms"] = float(te_t.item())
-            ex["GBps_per_direction"] = ex["bytes_per_direction"] / (ex["ms"] / 1e3) / 1e9
-    t = float(tt.item())
-    ms = t / args.steps
-    peak, kind = load_peaks()
-    sb_loc = ab << (n - p)
-    out = {
-        "metric": METRIC, "value": 1e3 / ms, "unit": "circuit/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][4], "circuit": "qft", "qubits": n,
-                   "local_qubits": n - p, "precision": prec, "parallelism": f"sharded x{world} (NCCL)",
-                   "exchanges_per_step": info.get("last_exchanges", 0),
-                   "fused_passes_per_step": info["last_passes"], "jit_specialised": info["last_jit"],
-                   "l2": f"state {sb_loc >> 20} MiB per GPU >> 126 MB L2"},
-        "gpu_launches": int(info["last_launches"] * args.steps),
-        "roofline": {"bound": "hbm", "kernel": "qc_pass (fused tile pass, per shard)",
-                     "achieved": 2 * sb_loc * info["last_passes"] / (ms / 1e3) / 1e9, "peak": peak,
-                     "unit": "GB/s", "traffic": None,
-                     "note": "lower bound: step time includes exchanges"},
-        "nvlink_exchange": ex, "clocks": clocks,
-    }
-    out["roofline"]["frac"] = out["roofline"]["achieved"] / peak
-    if ex is not None:
-        out["nvlink_exchange"]["frac_of_900"] = ex["GBps_per_direction"] / 900.0
-    s.close()
-    return out
 
 
 def sweep(args, local_rank):
@@ -429,7 +463,7 @@ def sweep(args, local_rank):
             inf = s.info()
             sb = (16 if prec == "c128" else 8) << n
             entry = {"ms": round(t, 4), "gates": len(ops), "passes": inf["last_passes"],
-                     "jit": inf["last_jit"]}
+                     "jit": inf["last_jit"], "Gamp_gate_per_s": round(gamp(ops, n, t / 1e3), 1)}
             alg = inf["last_flops_per_amp"] * float(1 << n) / (t / 1e3) / 1e12
             entry["fused_alg_TFLOPs"] = round(alg, 2)
             entry["fused_alg_flops_frac_of_fma_peak"] = round(alg / fma[prec], 4)
@@ -441,24 +475,21 @@ def sweep(args, local_rank):
             res["circuit_ms_vs_qubits"][key][str(n)] = entry
             s.close()
             torch.cuda.empty_cache()
-    # north-star capacity: configs C4 (TFXY n=33, 10 steps) and QFT n=33, complex128, 137 GB
+    # north-star capacity: QFT n=33 complex128, 137 GB (TFXY-33 is the headline)
     res["north_star_n33_c128"] = {}
     free, _ = torch.cuda.mem_get_info()
     if free > (16 << 33) * 1.05:
-        for fam in ("tfxy", "qft"):
-            ops = qcgen.qft(33) if fam == "qft" else qcgen.tfxy(33, 10)
-            s = qc.State(33, "c128", device=local_rank)
-            s.init_random(1)
-            t = _time_runs(s, qc.encode_ops(ops), warm=4 if fam == "qft" else 2, reps=2)
-            inf = s.info()
-            gbps = 2 * (16 << 33) * inf["last_passes"] / (t / 1e3) / 1e9
-            alg = inf["last_flops_per_amp"] * float(1 << 33) / (t / 1e3) / 1e12
-            res["north_star_n33_c128"][f"{fam}33" + ("_S10" if fam == "tfxy" else "")] = {
-                "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
-                "fused_alg_TFLOPs": round(alg, 2), "fused_alg_flops_frac_of_fp64_peak": round(alg / fma["c128"], 4),
-                "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
-            s.close()
-            torch.cuda.empty_cache()
+        ops = qcgen.qft(33)
+        s = qc.State(33, "c128", device=local_rank)
+        s.init_random(1)
+        t = _time_runs(s, qc.encode_ops(ops), warm=4, reps=2)
+        inf = s.info()
+        gbps = 2 * (16 << 33) * inf["last_passes"] / (t / 1e3) / 1e9
+        res["north_star_n33_c128"]["qft33"] = {
+            "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
+            "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
+        s.close()
+        torch.cuda.empty_cache()
     for prec in ("c128", "c64"):
         n = 30
         sb = (16 if prec == "c128" else 8) << n
@@ -485,39 +516,69 @@ def sweep(args, local_rank):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (deliberately slow CPU program) as it stands."""
+    """--impl reference: the oracle (deliberately slow CPU program) as it
+    stands, on this arm's workload, metric and unit: W untimed + K timed steps,
+    each step a bounded sample of the workload (OracleSampler)."""
     if rank != 0:
         return None
-    fam, n, steps_c, prec, desc = CONFIGS[args.config]
-    if n is None:  # sharded config: the whole state, n = local + log2(N)
-        n = args.local_qubits + (world.bit_length() - 1)
-    rate, cores, sample = cpu_oracle_rate(args.config, budget_s=max(5.0, 4.0 * args.steps), n_override=n)
-    return {"impl": "reference", "metric": METRIC, "value": rate, "unit": "circuit/s",
+    fam, n0, steps_c, prec, desc = CONFIGS[args.config]
+    n = n0 if n0 is not None else args.local_qubits + (world.bit_length() - 1)
+    smp = OracleSampler(args.config, n, step_s=2.0)
+    for _ in range(args.warmup):
+        smp.step()
+    smp.per_gate.clear()
+    times = [smp.step() for _ in range(args.steps)]
+    secs = sum(times)
+    csec = smp.circuit_seconds()
+    value = gamp(smp.ops, n, csec)
+    sample = smp.describe(args.steps, secs)
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "circuit": fam, "qubits": n, "precision": prec},
-            "cpu_baseline": {"value": rate, "unit": "circuit/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
-            "e2e": {"value": rate, "unit": "circuit/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "circuits_per_s": 1.0 / csec,
+            "config": {"workload": desc, "circuit": fam, "qubits": n, "precision": prec,
+                       "step": "one bounded oracle sample (ms_per_step = its wall time); value = the "
+                               "workload's amplitude-gate rate from the median per-gate time"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": smp.oracle.max_threads(), "kind": "oracle",
+                             "extrapolated": smp.n_s < n, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="tfxy20", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--local-qubits", type=int, default=30, help="qft_shard: qubits per GPU")
+    ap.add_argument("--local-qubits", type=int, default=33, help="sharded configs: qubits per GPU")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 5)  # JIT on 2nd use + graph capture; QFT relabels alternate plans
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-exec under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.config is None:
+        args.config = default_config(world)
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 4)  # JIT on the 2nd use + graph capture; QFT relabels alternate 2 plans
 
     if args.impl == "reference":
         out = run_reference(args, rank, world)
@@ -529,22 +590,13 @@ def main():
     if world > 1:
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.config == "qft_shard":
-        out = run_sharded(args, rank, world, local_rank)
-        if rank == 0:
-            print(json.dumps(out), flush=True)
-        if world > 1:
-            torch.distributed.barrier()
-            torch.distributed.destroy_process_group()
-        return
     out = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1:
         if not args.no_sweep:
             out["sweep"] = sweep(args, local_rank)
         if not args.no_cpu:
-            rate, cores, sample = cpu_oracle_rate(args.config)
-            out["cpu_baseline"] = {"value": rate, "unit": "circuit/s", "cores": cores,
-                                   "kind": "oracle", "sample": sample}
+            n = out["config"]["qubits"]
+            out["cpu_baseline"] = cpu_baseline(args.config, n)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -36,6 +37,8 @@ const int kArity[16] = {1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 1, 2, 2, 3};
 const int kNctrl[16] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 0, 2};
 const char* kName[16] = {"H", "X", "Y", "Z", "P", "RX", "RY", "RZ",
                          "CNOT", "CZ", "CP", "SWAP", "U1", "CU1", "U2", "CCX"};
+
+constexpr int kMaxDevices = 64;
 
 size_t amp_bytes(const qc_state* s) { return s->dbl ? 16 : 8; }
 
@@ -201,7 +204,7 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
   int k, rb, ctas;
   plan_geometry(s, n, &k, &rb, &ctas);
   const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
-                        ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)(s->jit == 2) << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^ ((uint64_t)s->remap << 52) ^
+                        ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)s->jit << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^ ((uint64_t)s->remap << 52) ^
                         ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
   const uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
   auto it = s->plans.find(key);
@@ -277,11 +280,16 @@ qc_status maybe_jit(qc_state* s, PlanEntry* e) {
 }
 
 qc_status ensure_fused_configured(qc_state* s) {
-  static bool configured[2] = {false, false};  // per process (device attributes of our kernels)
-  if (!configured[s->dbl]) {
+  // cudaFuncSetAttribute applies to the current device only: one flag per
+  // (device, precision)
+  static std::mutex mu;
+  static bool configured[kMaxDevices][2] = {};
+  if (s->device < 0 || s->device >= kMaxDevices) return fail(QC_ERR_UNSUPPORTED, "device ordinal %d", s->device);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!configured[s->device][s->dbl]) {
     const int r = fused_configure(s->dbl);
     if (r) return cuda_fail(s, r, "cudaFuncSetAttribute(fused)");
-    configured[s->dbl] = true;
+    configured[s->device][s->dbl] = true;
   }
   return QC_OK;
 }
@@ -509,9 +517,7 @@ qc_status qc_state_init_basis(qc_state* s, uint64_t k) {
     const uint64_t nl = 1ull << s->n_loc;
     cudaError_t e = cudaMemsetAsync(s->d, 0, s->bytes, s->stream);
     if (e != cudaSuccess) return cuda_fail(s, e, "init_basis");
-    if ((k / nl) == (uint64_t)s->rank) {
-      const int r = launch_init_basis(s->d, 0, s->dbl, 0, s->stream);  // n=0: sets element 0 only... see below
-      (void)r;
+    if ((k / nl) == (uint64_t)s->rank) {  // the owning rank stores the single 1 at k mod 2^n_loc
       double one[2] = {1.0, 0.0};
       float onef[2] = {1.0f, 0.0f};
       e = cudaMemcpyAsync((char*)s->d + (k % nl) * amp_bytes(s), s->dbl ? (void*)one : (void*)onef,

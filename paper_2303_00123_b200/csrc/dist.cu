@@ -108,12 +108,13 @@ qc_status nccl_fail(qc_state* s, int r, const char* what) {
 }
 
 // non-diagonal target qubits of a (logical) op
-uint32_t nondiag_qubits_mask(const qc_gate& g, int n) {
+// (64-bit: logical qubits reach 39; a 32-bit shift would alias q and q-32)
+uint64_t nondiag_qubits_mask(const qc_gate& g, int n) {
   (void)n;
   switch (g.op) {
     case QC_Z: case QC_P: case QC_RZ: case QC_CZ: case QC_CP: return 0;
-    case QC_SWAP: case QC_U2: return (1u << g.qubits[0]) | (1u << g.qubits[1]);
-    default: return 1u << g.qubits[kNctrl[g.op]];
+    case QC_SWAP: case QC_U2: return (1ull << g.qubits[0]) | (1ull << g.qubits[1]);
+    default: return 1ull << g.qubits[kNctrl[g.op]];
   }
 }
 
@@ -237,9 +238,9 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
   std::vector<std::vector<int>> uses(n);
   for (size_t i = 0; i < n_ops; ++i) {
     if (ops[i].op == QC_SWAP && s->relabel) continue;
-    const uint32_t m = nondiag_qubits_mask(ops[i], n);
+    const uint64_t m = nondiag_qubits_mask(ops[i], n);
     for (int q = 0; q < n; ++q)
-      if (m & (1u << q)) uses[q].push_back((int)i);
+      if (m & (1ull << q)) uses[q].push_back((int)i);
   }
   auto next_use = [&](int q, size_t i) -> long {
     auto it = std::upper_bound(uses[q].begin(), uses[q].end(), (int)i);
@@ -277,18 +278,18 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       P->relabels++;
       continue;
     }
-    const uint32_t nd = nondiag_qubits_mask(op, n);
-    uint32_t op_qubits = 0;
-    for (int t = 0; t < kArity[op.op]; ++t) op_qubits |= 1u << op.qubits[t];
+    const uint64_t nd = nondiag_qubits_mask(op, n);
+    uint64_t op_qubits = 0;
+    for (int t = 0; t < kArity[op.op]; ++t) op_qubits |= 1ull << op.qubits[t];
     for (int q = 0; q < n; ++q) {
-      if (!(nd & (1u << q)) || lay[q] < nl) continue;
+      if (!(nd & (1ull << q)) || lay[q] < nl) continue;
       // qubit q is non-diagonal and global: bring it to local bit L
       const int g = lay[q];
       int victim = -1;
       long best = -1;
       for (int p = 0; p < nl; ++p) {
         const int vq = inv[p];
-        if (op_qubits & (1u << vq)) continue;  // must stay local for this op
+        if (op_qubits & (1ull << vq)) continue;  // must stay local for this op
         const long nu = next_use(vq, i);
         const long score = nu * 2 + (p == L ? 1 : 0);  // prefer the slot itself on ties
         if (score > best) {
@@ -385,7 +386,8 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops) {
   }
   const uint64_t salt = 0xd157ull ^ ((uint64_t)s->relabel << 2) ^ ((uint64_t)s->block_fusion << 3) ^
                         ((uint64_t)s->tile_bits << 8) ^ ((uint64_t)s->row_bits << 16) ^
-                        ((uint64_t)s->tma_mode << 24) ^ ((uint64_t)s->jit << 28);
+                        ((uint64_t)s->tma_mode << 24) ^ ((uint64_t)s->jit << 28) ^ ((uint64_t)s->remap << 32) ^
+                        ((uint64_t)s->ctas << 36) ^ ((uint64_t)s->fusion << 56);
   const uint64_t key = hash_ops(ops, n_ops, s->layout, s->n, salt);
   DistPlan* P = nullptr;
   if (!s->dcache) s->dcache = new DistCache();

@@ -110,3 +110,35 @@ def test_schedule_makes_every_target_local():
             assert g >= n - p and l == n - p - 1
         gates = sum(s[3] for s in steps if s[0] == 0)
         assert gates >= len(qcgen.qft(n)) - n // 2  # SWAPs are relabels
+
+
+@pytest.mark.parametrize("n,world", [(33, 2), (34, 4), (36, 8), (36, 16), (40, 8)])
+def test_schedule_64bit_qubit_masks(n, world):
+    """Qubits >= 32 must not alias qubit q-32 (64-bit masks): gates whose
+    non-diagonal targets are local need no exchange at any n; a single
+    non-diagonal gate on a global qubit needs exactly one, on its rank bit."""
+    p = world.bit_length() - 1
+    local_ops = [qcgen.Op("H", (q,)) for q in range(p, n)] + \
+                [qcgen.Op("CNOT", (q, q + 1)) for q in range(p, n - 1)] + \
+                [qcgen.Op("RZ", (q,), theta=0.3) for q in range(n)]  # diagonal: never exchanged
+    steps, lay = qc.debug_dist_schedule(n, world, local_ops)
+    assert [s for s in steps if s[0] == 1] == []
+    assert lay == [n - 1 - q for q in range(n)]
+    for gq in range(p):
+        steps, _ = qc.debug_dist_schedule(n, world, [qcgen.Op("H", (33 if n > 33 else n - 1,)),
+                                                     qcgen.Op("H", (gq,))])
+        ex = [s for s in steps if s[0] == 1]
+        assert len(ex) == 1 and ex[0][1] == n - 1 - gq and ex[0][2] == n - p - 1
+
+
+def test_schedule_exchange_counts_at_full_size():
+    """Exchange counts of the north-star sharded workloads (C5, and TFXY at the
+    sizes of the scaling grid) after the 64-bit-mask fix; the round-1 32-bit
+    masks scheduled 6 / 62 / 42 (VERDICT r01 recomputation: 4 / 51 / 31)."""
+    def count(n, world, ops):
+        steps, lay = qc.debug_dist_schedule(n, world, ops)
+        assert sorted(lay) == list(range(n))
+        return sum(1 for s in steps if s[0] == 1)
+    assert count(36, 8, qcgen.qft(36)) == 4
+    assert count(33, 8, qcgen.tfxy(33, 10)) == 51
+    assert count(35, 4, qcgen.tfxy(35, 10)) == 31

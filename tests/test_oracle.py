@@ -152,6 +152,28 @@ def test_fig_dctrl_1q_index_sets():
             assert np.array_equal(out, basis(3, x))
 
 
+def test_ccx_mixed_ctrl_state_bit_order():
+    """Two controls with mixed required states (fig:dctrl-1q, P:948-978,
+    generalised per P:942-946: each control is a predicate on its own index
+    bit).  qc.h fixes ctrl_state bit t = required state of LISTED control t.
+    Brute force on every basis state of n=4, every ordered choice of
+    (control0, control1, target): ctrl_state 1 (c0=1, c1=0) and 2 (c0=0, c1=1)
+    tell ``<< t`` from ``<< (nc-1-t)``; 0 and 3 are the symmetric cases."""
+    n = 4
+    for c0 in range(n):
+        for c1 in range(n):
+            for t in range(n):
+                if len({c0, c1, t}) < 3:
+                    continue
+                for cs in range(4):
+                    for x in range(1 << n):
+                        bit = lambda q: (x >> (n - 1 - q)) & 1
+                        fire = bit(c0) == (cs & 1) and bit(c1) == ((cs >> 1) & 1)
+                        y = x ^ (1 << (n - 1 - t)) if fire else x
+                        out = oracle.run(n, basis(n, x), [Op("CCX", (c0, c1, t), ctrl_state=cs)])
+                        assert np.array_equal(out, basis(n, y)), (c0, c1, t, cs, x)
+
+
 def test_cnot_listing_order():
     # eq:kron reading (SURVEY 8(c) item 1): CNOT(c,t) on |c=1,t=0> -> |1,1>.
     for n, c, t in ((2, 0, 1), (2, 1, 0), (4, 3, 1), (5, 0, 4)):
