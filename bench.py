@@ -375,7 +375,8 @@ def run_ours(args, rank, world, local_rank):
     avg_launch_ms = ms_per_step / max(launches_per_step, 1)
     achieved = 2 * shard_bytes / (avg_launch_ms / 1e3) / 1e9
     fma_peak, fma_src = derived_fma_peak(prec, local_rank)
-    flops = info["last_flops_per_amp"] * float(1 << n_loc)
+    # last_flops_per_amp sums every pass of the plan: per launch = that / passes
+    flops = info["last_flops_per_amp"] * float(1 << n_loc) / max(passes, 1)
     alu_achieved = flops / (avg_launch_ms / 1e3) / 1e12
     traffic, traffic_src = load_traffic(args.config if world == 1 else f"{fam}{n_loc}")
     hbm_view = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -384,7 +385,8 @@ def run_ours(args, rank, world, local_rank):
                 "frac": alu_achieved / fma_peak, "peak_source": fma_src, "flops_per_launch": flops,
                 "flops_note": "algorithmic flops of the fused plan's ops (qc_info.last_flops_per_amp: complex "
                               "arithmetic, general cmul 6 / cmac 8 flops, unit coefficients free, x fraction of "
-                              "amplitudes touched) x 2^n_local (one pass)",
+                              "amplitudes touched, summed over the plan's passes) x 2^n_local / passes "
+                              "(the mean launch)",
                 "unfused_gate_flops_per_step": circuit_flops(ops, n)}
     # binding roof: the larger fraction (ALU for block-fused TFXY, HBM for QFT)
     main_view = alu_view if alu_view["frac"] > hbm_view["frac"] else hbm_view

@@ -152,6 +152,14 @@ uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint6
   return h;
 }
 
+// Per-pass FP64 budget of the planner (flops per amplitude, plan_fused).
+double pass_flops_budget(bool dbl) {
+  const char* e = getenv("QC_PASS_FLOPS");
+  if (e) return atof(e);
+  (void)dbl;
+  return 0;
+}
+
 void plan_geometry(const qc_state* s, int n_plan, int* k_out, int* rb_out, int* ctas_out) {
   int k = s->tile_bits ? s->tile_bits : (s->dbl ? 12 : 13);
   if (s->dbl && k > 12) k = 12;  // two 2^k tiles (one per compute group) must fit in smem
@@ -177,7 +185,7 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
   e->fused_gates = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap);
+  FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap, pass_flops_budget(s->dbl));
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
   e->perm = fp.perm;
   e->flops_per_amp = plan_flops_per_amp(fp);
@@ -816,7 +824,7 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates, ~0ull) : gates;
   out->blocks = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  FusedPlan fp = plan_fused(n, k, rb, blocks, remap != 0);
+  FusedPlan fp = plan_fused(n, k, rb, blocks, remap != 0, pass_flops_budget(dbl));
   if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
   out->remap_swaps = fp.remap_swaps;
   out->flops_per_amp = plan_flops_per_amp(fp);

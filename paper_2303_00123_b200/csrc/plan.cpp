@@ -35,6 +35,21 @@ uint64_t target_mask(const PGate& g) {
 }
 uint64_t need_mask(const PGate& g) { return g.kind == GK::DIAG1 ? 0ull : target_mask(g); }
 
+// Algorithmic flops per state amplitude of one (block-fused) gate inside a
+// fused pass, as plan_flops_per_amp counts them (complex multiply 6, multiply-
+// accumulate 8), halved per control bit.  Used for the per-pass FP64 budget.
+double gate_flops(const PGate& g) {
+  const double ctrl = std::ldexp(1.0, -popc(g.cmask));
+  switch (g.kind) {
+    case GK::DENSE1: return 14 * ctrl;
+    case GK::DIAG1: return (g.d0_is_one ? 3 : 6) * ctrl;
+    case GK::DENSE2: return 30 * ctrl;
+    case GK::SPARSE2: return 14 * ctrl;
+    case GK::DIAG2: return 6 * ctrl;
+    default: return 0;  // permutations / swaps: register moves
+  }
+}
+
 size_t blob_estimate(const PGate& g) {
   if (g.kind == GK::DIAG1) return 48;
   if (pgate_is_two(g)) return 48 + 16 * 16;
@@ -655,7 +670,7 @@ std::vector<std::pair<int, int>> remap_swaps(const std::vector<int>& perm, uint6
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, bool remap) {
+FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, bool remap, double flops_budget) {
   FusedPlan plan;
   std::vector<PGate> gates = gates_in;  // bits relabelled by in-pass remap swaps
   plan.perm.resize(n);
@@ -670,6 +685,8 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
     uint64_t T = rows;
     uint64_t blocked = 0;
     size_t bytes = 0;
+    double flops = 0;  // FP64 budget: past the HBM/FP64 ridge a pass is ALU-bound, and the
+                       // gates it still takes cost more time than the next pass's round trip
     std::vector<int> taken, deferred;
     for (int gi : remaining) {
       const PGate& g = gates[gi];
@@ -685,9 +702,12 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
       }
       const uint64_t nt = T | need_mask(g);
       const size_t est = blob_estimate(g);
-      if (popc(nt) <= k && bytes + est <= kBlobMax - 4096) {
+      const double gf = gate_flops(g);
+      if (popc(nt) <= k && bytes + est <= kBlobMax - 4096 &&
+          (flops_budget <= 0 || taken.empty() || flops + gf <= flops_budget)) {
         T = nt;
         bytes += est;
+        flops += gf;
         taken.push_back(gi);
       } else {
         blocked |= all;
@@ -777,6 +797,10 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
   }
   for (int p = 0; p < n; ++p)
     if (plan.perm[p] != p) plan.ok = false;  // (cannot happen: every pass fixes >= 1 move)
+  if (getenv("QC_PLAN_DEBUG"))
+    for (size_t i = 0; i < plan.passes.size(); ++i)
+      fprintf(stderr, "pass %zu: subs %zu ops %zu flops/amp %.1f\n", i, plan.passes[i].subs.size(),
+              plan.passes[i].ops.size(), pass_flops_per_amp(plan.passes[i]));
   return plan;
 }
 
@@ -786,13 +810,13 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
 // it 2), times the fraction of amplitudes each op touches (predicates halve
 // it per bit, identity rows and the d0 = 1 half of a diagonal are skipped).
 // The ALU roofline of bench.py divides this work by the pass time.
-double plan_flops_per_amp(const FusedPlan& plan) {
+double pass_flops_per_amp(const FusedPassPlan& pp) {
   auto unit = [](cd z) {
     return (std::abs(z.imag()) == 0.0 && std::abs(z.real()) == 1.0) ||
            (z.real() == 0.0 && std::abs(z.imag()) == 1.0);
   };
   double total = 0;
-  for (const auto& pp : plan.passes)
+  {
     for (const auto& o : pp.ops) {
       if (o.folded) continue;
       const FHdr& h = o.h;
@@ -819,6 +843,13 @@ double plan_flops_per_amp(const FusedPlan& plan) {
         total += 6.0 * ((h.flags & 1) || !o.sterms.empty() ? 1.0 : 0.5) * pred;
       }
     }
+  }
+  return total;
+}
+
+double plan_flops_per_amp(const FusedPlan& plan) {
+  double total = 0;
+  for (const auto& pp : plan.passes) total += pass_flops_per_amp(pp);
   return total;
 }
 

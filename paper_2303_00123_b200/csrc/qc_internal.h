@@ -90,9 +90,13 @@ struct FusedPlan {
 
 // Planner (plan.cpp).  k = tile bits (<= n), returns passes covering all gates.
 // remap: passes may end with swaps of row bits and tile bits (plan.perm).
-FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates, bool remap = false);
+// flops_budget > 0: a pass stops taking gates once their algorithmic flops per
+// amplitude (gate_flops) would exceed it (the HBM/ALU ridge of a pass).
+FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates, bool remap = false,
+                     double flops_budget = 0);
 // Algorithmic flops per amplitude of the fused plan (ALU roofline numerator).
 double plan_flops_per_amp(const FusedPlan& plan);
+double pass_flops_per_amp(const FusedPassPlan& pp);
 // Pack the plan into one device blob for precision T (fills desc.blob_*).
 std::vector<uint8_t> pack_plan(FusedPlan& plan, bool dbl);
 
