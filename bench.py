@@ -517,6 +517,33 @@ def sweep(args, local_rank):
     return res
 
 
+def cpu_omp_curve(budget_s=40.0):
+    """The paper's CPU program (libqc_omp.so: Algs. 1-3, one OpenMP parallel
+    loop per gate) -- circuit time vs qubits on this host's cores, the
+    CPU side of the paper's CPU-vs-GPU experiments.  Bounded: sizes
+    are skipped once the budget is spent."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    import qcgen
+    from paper_2303_00123_b200 import cpu_omp
+    res = {"threads": cpu_omp.qc_omp_max_threads(), "cpu": cpu_model(),
+           "omp_proc_bind": os.environ.get("OMP_PROC_BIND"), "ms": {}}
+    cpu_omp.qc_omp_run(12, "c128", qcgen.random_state(12), qcgen.qft(12))  # thread-pool start-up
+    t_start = time.perf_counter()
+    for fam, prec, ns in (("qft", "c128", (16, 20, 22, 24)), ("qft", "c64", (20, 24)),
+                          ("tfxy", "c128", (16, 20, 22))):
+        key = f"{fam}_{prec}" + ("_S10" if fam == "tfxy" else "")
+        res["ms"][key] = {}
+        for n in ns:
+            if time.perf_counter() - t_start > budget_s:
+                break
+            ops = qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, 10)
+            x = qcgen.random_state(n, precision=prec)
+            t0 = time.perf_counter()
+            cpu_omp.qc_omp_run(n, prec, x, ops)
+            res["ms"][key][str(n)] = round((time.perf_counter() - t0) * 1e3, 2)
+    return res
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle (deliberately slow CPU program) as it
     stands, on this arm's workload, metric and unit: W untimed + K timed steps,
@@ -599,6 +626,7 @@ def main():
         if not args.no_cpu:
             n = out["config"]["qubits"]
             out["cpu_baseline"] = cpu_baseline(args.config, n)
+            out["cpu_omp_paper_program"] = cpu_omp_curve()
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -78,7 +78,9 @@ typedef enum {
 typedef enum {
     QC_H = 0, QC_X = 1, QC_Y = 2, QC_Z = 3, QC_P = 4, QC_RX = 5, QC_RY = 6, QC_RZ = 7,
     QC_CNOT = 8, QC_CZ = 9, QC_CP = 10, QC_SWAP = 11,
-    QC_U1 = 12, QC_CU1 = 13, QC_U2 = 14, QC_CCX = 15
+    QC_U1 = 12, QC_CU1 = 13, QC_U2 = 14, QC_CCX = 15,
+    QC_MGATE = 16   /* generic gate: qubits[0] = index into the qc_mgate table of
+                       qc_run_circuit_ex (other fields ignored, flags must be 0) */
 } qc_op;
 
 #define QC_CTRL_ONES 0xFFFFFFFFu  /* default: every control must be |1> */
@@ -107,9 +109,19 @@ typedef enum {
     QC_OPT_ROW_BITS = 7,      /* 0 (default): auto; else contiguous row bits of a fused tile */
     QC_OPT_TMA_MODE = 8,      /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
                                  request); 1: one cp.async.bulk per row                      */
-    QC_OPT_REMAP = 9          /* 1 (default): a fused pass may end by swapping row bits with
+    QC_OPT_REMAP = 9,         /* 1 (default): a fused pass may end by swapping row bits with
                                  tile bits the next pass needs (a relabel, like SWAP);
                                  0: the row bits keep their qubits                           */
+    QC_OPT_EXCHANGE = 10      /* NCCL-sharded states, qubit-swap exchange backend (collective:
+                                 set the same value on every rank):
+                                 0 (default): NCCL send/recv of 256 MiB chunks into two
+                                   ping-pong staging buffers on a second stream, each chunk's
+                                   copy into place overlapping the next chunk's transfer;
+                                 1: peer-to-peer -- every rank maps the others' state buffers
+                                   (CUDA IPC handles all-gathered over NCCL) and one kernel
+                                   per run swaps the two halves directly over NVLink (loads +
+                                   stores, no staging copy); the pair splits each run in two
+                                   and brackets the kernel with a pairwise NCCL token barrier */
 } qc_option;
 
 /* Counters of the most recent qc_run_circuit / qc_apply_gate. */
@@ -137,6 +149,28 @@ typedef struct qc_info {
                                   plan's fused ops (complex arithmetic counted;
                                   the ALU roofline numerator, qc_debug.h)      */
 } qc_info;
+
+/* Generic gate: any number of controls and a dense
+ * 2^k x 2^k matrix on k = n_targ <= 4 targets.  P:942-946 -- every further
+ * qubit is one more inserted index bit ("2 additional bit masks")
+ * -- a doubly controlled gate updates only the block where both controls hold
+ * (here: every control t equals bit t of ctrl_state).  The embedded operator
+ * over the listed qubits is the identity except that block, which holds the
+ * matrix; matrix rows/columns are big-endian over the listed TARGETS (first
+ * target = most significant index bit, eq:kron P:407-412, reading R1).
+ * Exact structure is detected (a diagonal / permutation 2x2 runs as a phase /
+ * move, X under controls is bit-exact).  88 bytes, 8-byte aligned. */
+#define QC_MGATE_MAX_QUBITS 16
+#define QC_MGATE_MAX_TARGETS 4
+typedef struct qc_mgate {
+    int32_t n_ctrl;            /* controls, listed first: 0..15                    */
+    int32_t n_targ;            /* targets after them: 1..4                          */
+    int32_t qubits[QC_MGATE_MAX_QUBITS];  /* distinct, in [0,n); past n_ctrl+n_targ ignored */
+    uint32_t ctrl_state;       /* bit t = required state of listed control t        */
+    uint32_t flags;            /* reserved, must be 0                               */
+    const double* matrix;      /* 2^k x 2^k complex, interleaved re,im, row-major;
+                                  borrowed for the call (copied before return)     */
+} qc_mgate;
 
 /* ---------------------------------------------------------------- lifetime */
 
@@ -207,6 +241,20 @@ qc_status qc_apply_gate(qc_state* s, qc_op op, const int* qubits, const double* 
  * planner groups gates into fused tile passes (one HBM round trip each);
  * otherwise one kernel per gate.  Enqueued; returns without waiting. */
 qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops);
+
+/* One generic gate with its own per-gate kernel (no fusion): validated
+ * (controls + targets distinct and in range, 1 <= n_targ <= 4, n_ctrl +
+ * n_targ <= 16, finite matrix, flags 0), then enqueued. */
+qc_status qc_apply_mgate(qc_state* s, const qc_mgate* g);
+
+/* qc_run_circuit with generic gates: an op with op == QC_MGATE stands for
+ * mgates[qubits[0]] (0 <= qubits[0] < n_mgates).  Same semantics, fusion,
+ * plan caching (keyed by the referenced gates' contents) and all-or-nothing
+ * validation as qc_run_circuit; mgates and their matrices are borrowed for
+ * the call only.  qc_run_circuit(s, ops, n) == qc_run_circuit_ex(s, ops, n,
+ * NULL, 0). */
+qc_status qc_run_circuit_ex(qc_state* s, const qc_gate* ops, size_t n_ops,
+                            const qc_mgate* mgates, size_t n_mgates);
 
 /* ------------------------------------------------------------------ I/O */
 

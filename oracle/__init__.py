@@ -55,6 +55,9 @@ def lib():
         L.orc_embed.restype = ctypes.c_int
         L.orc_embed.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_run_general.restype = ctypes.c_int64
+        L.orc_run_general.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_int64, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -78,16 +81,55 @@ def encode(ops: Sequence) -> np.ndarray:
     return arr
 
 
+GOP_DTYPE = np.dtype([("nq", "<i4"), ("nctrl", "<i4"), ("q", "<i4", (16,)), ("ctrl_state", "<u4"),
+                      ("pad", "<i4"), ("m", "<u8")])
+assert GOP_DTYPE.itemsize == 88
+
+
+def _run_general(n: int, psi: np.ndarray, ops: Sequence, nthreads: int) -> None:
+    """Generic (MCU) gates through orc_run_general, in order."""
+    arr = np.zeros(len(ops), dtype=GOP_DTYPE)
+    keep = []
+    for i, op in enumerate(ops):
+        arr[i]["nq"] = len(op.qubits)
+        arr[i]["nctrl"] = op.nctrl
+        arr[i]["q"] = list(op.qubits) + [0] * (16 - len(op.qubits))
+        arr[i]["ctrl_state"] = op.ctrl_state
+        m = np.ascontiguousarray(np.asarray(op.matrix, dtype=np.complex128)).view(np.float64).reshape(-1)
+        keep.append(m)
+        arr[i]["m"] = m.ctypes.data
+    rc = lib().orc_run_general(n, psi.ctypes.data, arr.ctypes.data if len(arr) else None, len(arr),
+                               int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle rejected generic op list (code {rc})")
+
+
 def run(n: int, state: np.ndarray, ops: Sequence, nthreads: int = 0) -> np.ndarray:
-    """Apply ``ops`` to a copy of ``state`` (any complex dtype, exact up-cast)."""
+    """Apply ``ops`` to a copy of ``state`` (any complex dtype, exact up-cast).
+    Generic ``MCU`` ops go through orc_run_general, the rest through orc_run,
+    in list order."""
     psi = np.ascontiguousarray(np.asarray(state).astype(np.complex128))
     if psi.size != (1 << n):
         raise ValueError("state size != 2^n")
-    enc = encode(ops)
-    rc = lib().orc_run(n, psi.ctypes.data, enc.ctypes.data if len(enc) else None,
-                       len(enc), int(nthreads))
-    if rc != 0:
-        raise ValueError(f"oracle rejected op list (code {rc})")
+    ops = list(ops)
+    i = 0
+    while i < len(ops) or i == 0:
+        j = i
+        gen = i < len(ops) and ops[i].name == "MCU"
+        while j < len(ops) and (ops[j].name == "MCU") == gen:
+            j += 1
+        seg = ops[i:j]
+        if gen:
+            _run_general(n, psi, seg, nthreads)
+        else:
+            enc = encode(seg)
+            rc = lib().orc_run(n, psi.ctypes.data, enc.ctypes.data if len(enc) else None,
+                               len(enc), int(nthreads))
+            if rc != 0:
+                raise ValueError(f"oracle rejected op list (code {rc})")
+        if j == i:
+            break
+        i = j
     return psi
 
 

@@ -64,7 +64,90 @@ qc_status cuda_fail(qc_state* s, int e, const char* what) {
   return fail(QC_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)e));
 }
 
-qc_status validate_gate(int n, const qc_gate& g, size_t idx) {
+// A generic gate (qc_mgate) -> validated copy.
+qc_status copy_mgate(int n, const qc_mgate& g, size_t idx, MGate* out) {
+  if (g.flags != 0) return fail(QC_ERR_INVALID_ARG, "mgate %zu: flags must be 0", idx);
+  if (g.n_targ < 1 || g.n_targ > QC_MGATE_MAX_TARGETS)
+    return fail(QC_ERR_INVALID_ARG, "mgate %zu: n_targ=%d outside [1,%d]", idx, g.n_targ, QC_MGATE_MAX_TARGETS);
+  if (g.n_ctrl < 0 || g.n_ctrl + g.n_targ > QC_MGATE_MAX_QUBITS)
+    return fail(QC_ERR_INVALID_ARG, "mgate %zu: n_ctrl=%d (n_ctrl + n_targ <= %d)", idx, g.n_ctrl,
+                QC_MGATE_MAX_QUBITS);
+  const int nq = g.n_ctrl + g.n_targ;
+  for (int t = 0; t < nq; ++t) {
+    if (g.qubits[t] < 0 || g.qubits[t] >= n)
+      return fail(QC_ERR_INVALID_ARG, "mgate %zu: qubit %d out of range [0,%d)", idx, g.qubits[t], n);
+    for (int u = 0; u < t; ++u)
+      if (g.qubits[u] == g.qubits[t]) return fail(QC_ERR_INVALID_ARG, "mgate %zu: qubit %d repeated", idx, g.qubits[t]);
+  }
+  if (!g.matrix) return fail(QC_ERR_INVALID_ARG, "mgate %zu: matrix is NULL", idx);
+  const int d = 1 << g.n_targ;
+  out->n_ctrl = g.n_ctrl;
+  out->n_targ = g.n_targ;
+  std::memset(out->qubits, 0, sizeof out->qubits);
+  for (int t = 0; t < nq; ++t) out->qubits[t] = g.qubits[t];
+  out->ctrl_state = g.n_ctrl >= 32 ? g.ctrl_state : (g.ctrl_state & ((1u << g.n_ctrl) - 1u));
+  out->m.resize((size_t)d * d);
+  for (int e = 0; e < d * d; ++e) {
+    if (!std::isfinite(g.matrix[2 * e]) || !std::isfinite(g.matrix[2 * e + 1]))
+      return fail(QC_ERR_INVALID_ARG, "mgate %zu: matrix entry %d not finite", idx, e);
+    out->m[e] = cd(g.matrix[2 * e], g.matrix[2 * e + 1]);
+  }
+  return QC_OK;
+}
+
+std::vector<uint8_t> mtable_key(const qc_gate* ops, size_t n_ops, const MTable* mt) {
+  std::vector<uint8_t> k;
+  if (!mt) return k;
+  auto put = [&](const void* p, size_t b) {
+    const uint8_t* c = reinterpret_cast<const uint8_t*>(p);
+    k.insert(k.end(), c, c + b);
+  };
+  for (size_t i = 0; i < n_ops; ++i) {
+    if (ops[i].op != QC_MGATE) continue;
+    const MGate& g = (*mt)[(size_t)ops[i].qubits[0]];
+    put(&g.n_ctrl, sizeof g.n_ctrl);
+    put(&g.n_targ, sizeof g.n_targ);
+    put(g.qubits, sizeof(int) * (size_t)(g.n_ctrl + g.n_targ));
+    put(&g.ctrl_state, sizeof g.ctrl_state);
+    put(g.m.data(), sizeof(cd) * g.m.size());
+  }
+  return k;
+}
+
+int op_qubits(const qc_gate& g, const MTable* mt, int* out) {
+  if (g.op == QC_MGATE) {
+    const MGate& m = (*mt)[(size_t)g.qubits[0]];
+    for (int t = 0; t < m.n_ctrl + m.n_targ; ++t) out[t] = m.qubits[t];
+    return m.n_ctrl + m.n_targ;
+  }
+  for (int t = 0; t < kArity[g.op]; ++t) out[t] = g.qubits[t];
+  return kArity[g.op];
+}
+
+// Logical non-diagonal targets (a diagonal gate never needs its qubit local).
+uint64_t op_nondiag_mask(const qc_gate& g, const MTable* mt) {
+  switch (g.op) {
+    case QC_Z: case QC_P: case QC_RZ: case QC_CZ: case QC_CP: return 0;
+    case QC_SWAP: case QC_U2: return (1ull << g.qubits[0]) | (1ull << g.qubits[1]);
+    case QC_MGATE: {
+      const MGate& m = (*mt)[(size_t)g.qubits[0]];
+      if (m.n_targ == 1 && m.m[1] == cd(0) && m.m[2] == cd(0)) return 0;
+      uint64_t r = 0;
+      for (int t = m.n_ctrl; t < m.n_ctrl + m.n_targ; ++t) r |= 1ull << m.qubits[t];
+      return r;
+    }
+    default: return 1ull << g.qubits[kNctrl[g.op]];
+  }
+}
+
+qc_status validate_gate(int n, const qc_gate& g, size_t idx, const MTable* mt) {
+  if (g.op == QC_MGATE) {
+    if (g.flags != 0) return fail(QC_ERR_INVALID_ARG, "op %zu: flags must be 0", idx);
+    if (!mt || g.qubits[0] < 0 || (size_t)g.qubits[0] >= mt->size())
+      return fail(QC_ERR_INVALID_ARG, "op %zu (MGATE): index %d outside the mgate table (%zu)", idx, g.qubits[0],
+                  mt ? mt->size() : (size_t)0);
+    return QC_OK;
+  }
   if (g.op < 0 || g.op > 15) return fail(QC_ERR_INVALID_ARG, "op %zu: unknown op code %d", idx, g.op);
   if (g.flags != 0) return fail(QC_ERR_INVALID_ARG, "op %zu: flags must be 0", idx);
   const int k = kArity[g.op];
@@ -86,8 +169,50 @@ qc_status validate_gate(int n, const qc_gate& g, size_t idx) {
   return QC_OK;
 }
 
+// Generic gate -> physical-bit kernel class; the exact structure of a 2x2
+// target matrix picks the class (diagonal -> phase, X pattern -> move).
+PGate lower_mgate(const MGate& g, const int* layout) {
+  PGate p;
+  for (int t = 0; t < g.n_ctrl; ++t) {
+    const int b = layout[g.qubits[t]];
+    p.cmask |= 1ull << b;
+    if ((g.ctrl_state >> t) & 1u) p.cval |= 1ull << b;
+  }
+  const int* tq = g.qubits + g.n_ctrl;
+  const cd* M = g.m.data();
+  auto zero = [](cd z) { return z.real() == 0.0 && z.imag() == 0.0; };
+  auto one = [](cd z) { return z.real() == 1.0 && z.imag() == 0.0; };
+  if (g.n_targ == 1) {
+    p.t0 = layout[tq[0]];
+    if (zero(M[1]) && zero(M[2])) {
+      p.kind = GK::DIAG1;
+      p.m[0] = M[0];
+      p.m[1] = M[3];
+      p.d0_is_one = one(M[0]);
+    } else if (zero(M[0]) && zero(M[3]) && one(M[1]) && one(M[2])) {
+      p.kind = GK::PERM1;
+    } else {
+      p.kind = GK::DENSE1;
+      for (int i = 0; i < 4; ++i) p.m[i] = M[i];
+    }
+  } else if (g.n_targ == 2) {
+    p.kind = GK::DENSE2;
+    p.t0 = layout[tq[0]];
+    p.t1 = layout[tq[1]];
+    for (int i = 0; i < 16; ++i) p.m[i] = M[i];
+  } else {
+    p.kind = GK::DENSEK;
+    p.nt = g.n_targ;
+    for (int j = 0; j < g.n_targ; ++j) p.tk[j] = layout[tq[j]];
+    p.t0 = p.tk[0];
+    p.mk = std::make_shared<const std::vector<cd>>(g.m);
+  }
+  return p;
+}
+
 // Lower one validated gate to a physical-bit kernel class (DESIGN R4 matrices).
-PGate lower(const qc_gate& g, const int* layout) {
+PGate lower(const qc_gate& g, const int* layout, const MTable* mt) {
+  if (g.op == QC_MGATE) return lower_mgate((*mt)[(size_t)g.qubits[0]], layout);
   PGate p;
   const int nc = kNctrl[g.op];
   for (int t = 0; t < nc; ++t) {
@@ -185,6 +310,12 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
   e->fused_gates = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
+  // a tile holds the row bits plus every non-diagonal target of a gate: a
+  // generic gate's 3-4 targets may need narrower rows in a small tile
+  for (const PGate& g : blocks) {
+    const int need = g.kind == GK::DIAG1 ? 0 : std::popcount(pgate_targets(g));
+    if (rb + need > k) rb = std::max(1, k - need);
+  }
   FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap, pass_flops_budget(s->dbl));
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
   e->perm = fp.perm;
@@ -207,25 +338,28 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
 }
 
 // Build (or fetch) the fused plan for this op list and the current layout.
-qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** out) {
+qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* mt, PlanEntry** out) {
   const int n = s->n;
   int k, rb, ctas;
   plan_geometry(s, n, &k, &rb, &ctas);
   const uint64_t salt = ((uint64_t)s->fusion << 1) ^ ((uint64_t)s->relabel << 2) ^
                         ((uint64_t)s->block_fusion << 3) ^ ((uint64_t)s->jit << 4) ^ ((uint64_t)s->row_bits << 40) ^ ((uint64_t)s->tma_mode << 48) ^ ((uint64_t)s->remap << 52) ^
                         ((uint64_t)k << 8) ^ ((uint64_t)s->dbl << 16) ^ ((uint64_t)ctas << 20);
-  const uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
+  std::vector<uint8_t> mkey = mtable_key(ops, n_ops, mt);
+  uint64_t key = hash_ops(ops, n_ops, s->layout, n, salt);
+  for (uint8_t b : mkey) key = (key ^ b) * 0x100000001b3ull;
   auto it = s->plans.find(key);
   if (it != s->plans.end()) {
     PlanEntry* e = it->second.get();
     if (e->ops.size() == n_ops && std::memcmp(e->ops.data(), ops, n_ops * sizeof(qc_gate)) == 0 &&
-        std::memcmp(e->layout_in.data(), s->layout, n * sizeof(int)) == 0) {
+        e->mkey == mkey && std::memcmp(e->layout_in.data(), s->layout, n * sizeof(int)) == 0) {
       *out = e;
       return QC_OK;
     }
   }
   auto e = std::make_unique<PlanEntry>();
   e->ops.assign(ops, ops + n_ops);
+  e->mkey = std::move(mkey);
   e->layout_in.assign(s->layout, s->layout + n);
   // lower in order, applying SWAP relabels to a running layout
   int lay[64];
@@ -238,7 +372,7 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, PlanEntry** ou
       e->relabels++;
       continue;
     }
-    PGate g = lower(ops[i], lay);
+    PGate g = lower(ops[i], lay, mt);
     g.src_op = (int)i;
     gates.push_back(g);
   }
@@ -302,13 +436,13 @@ qc_status ensure_fused_configured(qc_state* s) {
   return QC_OK;
 }
 
-qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
+qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* mt) {
   {
     const qc_status c = ensure_fused_configured(s);
     if (c != QC_OK) return c;
   }
   PlanEntry* e = nullptr;
-  qc_status st = get_plan(s, ops, n_ops, &e);
+  qc_status st = get_plan(s, ops, n_ops, mt, &e);
   if (st != QC_OK) return st;
   e->uses++;
   s->last_graph = 0;
@@ -348,7 +482,7 @@ qc_status run_fused(qc_state* s, const qc_gate* ops, size_t n_ops) {
   return QC_OK;
 }
 
-qc_status run_unfused(qc_state* s, const qc_gate* ops, size_t n_ops) {
+qc_status run_unfused(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* mt) {
   int64_t launches = 0, relabels = 0;
   for (size_t i = 0; i < n_ops; ++i) {
     if (ops[i].op == QC_SWAP && s->relabel) {
@@ -356,7 +490,7 @@ qc_status run_unfused(qc_state* s, const qc_gate* ops, size_t n_ops) {
       ++relabels;
       continue;
     }
-    const PGate g = lower(ops[i], s->layout);
+    const PGate g = lower(ops[i], s->layout, mt);
     const int r = launch_gate(s->d, s->n, s->dbl, g, s->stream);
     if (r) return cuda_fail(s, r, "gate kernel launch");
     ++launches;
@@ -508,6 +642,10 @@ void qc_state_destroy(qc_state* s) {
   s->plans.clear();
   dist_release(s);
   if (s->d_xstage) cudaFree(s->d_xstage);
+  if (s->d_token) cudaFree(s->d_token);
+  for (cudaEvent_t e : s->xev)
+    if (e) cudaEventDestroy(e);
+  if (s->xstream) cudaStreamDestroy(s->xstream);
   if (s->own_mem && s->d) cudaFree(s->d);
   if (s->d_stage) cudaFree(s->d_stage);
   if (s->d_partial) cudaFree(s->d_partial);
@@ -569,15 +707,37 @@ qc_status qc_apply_gate(qc_state* s, qc_op op, const int* qubits, const double* 
   st = validate_gate(s->n, g, 0);
   if (st != QC_OK) return st;
   if (s->dist) return run_dist(s, &g, 1);
-  return run_unfused(s, &g, 1);
+  return run_unfused(s, &g, 1, nullptr);
 }
 
-qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops) {
+qc_status qc_apply_mgate(qc_state* s, const qc_mgate* mg) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  if (!mg) return fail(QC_ERR_INVALID_ARG, "mgate is NULL");
+  MTable mt(1);
+  st = copy_mgate(s->n, *mg, 0, &mt[0]);
+  if (st != QC_OK) return st;
+  qc_gate g;
+  std::memset(&g, 0, sizeof g);
+  g.op = QC_MGATE;
+  if (s->dist) return run_dist(s, &g, 1, &mt);
+  return run_unfused(s, &g, 1, &mt);
+}
+
+qc_status qc_run_circuit_ex(qc_state* s, const qc_gate* ops, size_t n_ops, const qc_mgate* mgates,
+                            size_t n_mgates) {
   qc_status st = check_state(s);
   if (st != QC_OK) return st;
   if (n_ops && !ops) return fail(QC_ERR_INVALID_ARG, "ops is NULL");
+  if (n_mgates && !mgates) return fail(QC_ERR_INVALID_ARG, "mgates is NULL");
+  MTable table(n_mgates);
+  for (size_t i = 0; i < n_mgates; ++i) {
+    st = copy_mgate(s->n, mgates[i], i, &table[i]);
+    if (st != QC_OK) return st;
+  }
+  const MTable* mt = n_mgates ? &table : nullptr;
   for (size_t i = 0; i < n_ops; ++i) {
-    st = validate_gate(s->n, ops[i], i);
+    st = validate_gate(s->n, ops[i], i, mt);
     if (st != QC_OK) return st;
   }
   s->last_gates = (int64_t)n_ops;
@@ -585,9 +745,13 @@ qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops) {
     s->last_passes = s->last_launches = s->last_relabels = 0;
     return QC_OK;
   }
-  if (s->dist) return run_dist(s, ops, n_ops);  // sharded: fused segments + exchanges
-  if (s->fusion && s->n >= kSlotBits) return run_fused(s, ops, n_ops);
-  return run_unfused(s, ops, n_ops);
+  if (s->dist) return run_dist(s, ops, n_ops, mt);  // sharded: fused segments + exchanges
+  if (s->fusion && s->n >= kSlotBits) return run_fused(s, ops, n_ops, mt);
+  return run_unfused(s, ops, n_ops, mt);
+}
+
+qc_status qc_run_circuit(qc_state* s, const qc_gate* ops, size_t n_ops) {
+  return qc_run_circuit_ex(s, ops, n_ops, nullptr, 0);
 }
 
 qc_status qc_state_sync(qc_state* s) {
@@ -750,6 +914,10 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       s->tma_mode = (int)v;
       break;
     case QC_OPT_REMAP: s->remap = v != 0; break;
+    case QC_OPT_EXCHANGE:
+      if (v < 0 || v > 1) return fail(QC_ERR_INVALID_ARG, "exchange must be 0 (NCCL) or 1 (P2P)");
+      s->xmode = (int)v;
+      break;
     case QC_OPT_JIT:
       if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "jit must be 0, 1 or 2");
       s->jit = (int)v;

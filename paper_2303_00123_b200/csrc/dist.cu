@@ -40,6 +40,7 @@ namespace qc {
 
 struct DistPlan {
   std::vector<qc_gate> ops;
+  std::vector<uint8_t> mkey;  // referenced generic gates' contents
   std::vector<int> layout_in, layout_out;
   struct Step {
     int kind = 0;  // 0: fused local segment, 1: exchange
@@ -71,6 +72,7 @@ struct Nccl {
   int (*group_start)() = nullptr;
   int (*group_end)() = nullptr;
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
   bool ok = false;
 };
@@ -94,10 +96,11 @@ Nccl& nccl() {
     QC_NSYM(group_start, "ncclGroupStart");
     QC_NSYM(group_end, "ncclGroupEnd");
     QC_NSYM(all_reduce, "ncclAllReduce");
+    QC_NSYM(all_gather, "ncclAllGather");
     QC_NSYM(error_string, "ncclGetErrorString");
 #undef QC_NSYM
     n.ok = n.get_unique_id && n.comm_init_rank && n.comm_destroy && n.send && n.recv && n.group_start &&
-           n.group_end && n.all_reduce;
+           n.group_end && n.all_reduce && n.all_gather;
   });
   return n;
 }
@@ -107,16 +110,6 @@ qc_status nccl_fail(qc_state* s, int r, const char* what) {
   return fail(QC_ERR_NCCL, "%s: %s", what, nccl().error_string ? nccl().error_string(r) : "nccl error");
 }
 
-// non-diagonal target qubits of a (logical) op
-// (64-bit: logical qubits reach 39; a 32-bit shift would alias q and q-32)
-uint64_t nondiag_qubits_mask(const qc_gate& g, int n) {
-  (void)n;
-  switch (g.op) {
-    case QC_Z: case QC_P: case QC_RZ: case QC_CZ: case QC_CP: return 0;
-    case QC_SWAP: case QC_U2: return (1ull << g.qubits[0]) | (1ull << g.qubits[1]);
-    default: return 1ull << g.qubits[kNctrl[g.op]];
-  }
-}
 
 }  // namespace
 
@@ -155,6 +148,9 @@ qc_status nccl_get_unique_id(void* out128) {
 void dist_release(qc_state* s) {
   delete s->dcache;
   s->dcache = nullptr;
+  for (int r = 0; r < (int)s->peers.size(); ++r)
+    if (r != s->rank && s->peers[r]) cudaIpcCloseMemHandle(s->peers[r]);
+  s->peers.clear();
   nccl_destroy(s);
 }
 
@@ -178,6 +174,106 @@ qc_status nccl_allreduce_sum(qc_state* s, double* host_value) {
   return QC_OK;
 }
 
+namespace {
+
+// Staging (bytes), the exchange stream and its events, created on first use.
+qc_status ensure_xresources(qc_state* s, size_t bytes) {
+  if (s->xstage_bytes < bytes) {
+    if (s->d_xstage) cudaFree(s->d_xstage);
+    s->d_xstage = nullptr;
+    s->xstage_bytes = 0;
+    cudaError_t e = cudaMalloc(&s->d_xstage, bytes);
+    if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "exchange staging (%zu B)", bytes);
+    s->xstage_bytes = bytes;
+  }
+  if (!s->xstream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking);
+    for (int i = 0; i < 5 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&s->xev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(s, e, "exchange stream");
+  }
+  return QC_OK;
+}
+
+// Collective, once per state: all-gather every rank's CUDA IPC handle of its
+// state buffer over NCCL and map the other ranks' buffers (peer access over
+// NVLink; cudaIpcMemLazyEnablePeerAccess).
+qc_status ensure_peers(qc_state* s) {
+  if (!s->peers.empty()) return QC_OK;
+  Nccl& N = nccl();
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, s->d);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaIpcGetMemHandle");
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  std::vector<cudaIpcMemHandle_t> all((size_t)s->world);
+  char* d = nullptr;
+  e = cudaMalloc(&d, hb * (size_t)(s->world + 1));
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaMalloc (IPC handles)");
+  e = cudaMemcpyAsync(d, &h, hb, cudaMemcpyHostToDevice, s->stream);
+  int r = e == cudaSuccess ? N.all_gather(d, d + hb, hb, kNcclUint8, s->nccl_comm, s->stream) : 0;
+  if (e == cudaSuccess && !r) e = cudaMemcpyAsync(all.data(), d + hb, hb * s->world, cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess && !r) e = cudaStreamSynchronize(s->stream);
+  cudaFree(d);
+  if (r) return nccl_fail(s, r, "ncclAllGather (IPC handles)");
+  if (e != cudaSuccess) return cuda_fail(s, e, "IPC handle exchange");
+  s->peers.assign((size_t)s->world, nullptr);
+  for (int q = 0; q < s->world; ++q) {
+    if (q == s->rank) {
+      s->peers[q] = s->d;
+      continue;
+    }
+    e = cudaIpcOpenMemHandle(&s->peers[q], all[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      s->peers.clear();
+      return cuda_fail(s, e, "cudaIpcOpenMemHandle");
+    }
+  }
+  if (!s->d_token) {
+    e = cudaMalloc(&s->d_token, 2 * sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaMalloc (token)");
+  }
+  return QC_OK;
+}
+
+// Stream-ordered pairwise barrier: a 1-int NCCL send/recv with the partner
+// completes only after the partner has enqueued (and its stream reached) the
+// matching call, i.e. after every earlier kernel on the partner's stream.
+qc_status pair_barrier(qc_state* s, int partner) {
+  Nccl& N = nccl();
+  int r = N.group_start();
+  if (!r) r = N.send(s->d_token, 1, kNcclUint8, partner, s->nccl_comm, s->stream);
+  if (!r) r = N.recv(s->d_token + 1, 1, kNcclUint8, partner, s->nccl_comm, s->stream);
+  const int r2 = N.group_end();
+  if (r || r2) return nccl_fail(s, r ? r : r2, "pair barrier");
+  return QC_OK;
+}
+
+// P2P exchange: the pair swaps my run with the partner's matching run in
+// place -- the lower rank the first half of every run, the upper rank the
+// second half -- with one kernel reading and writing both buffers (the
+// partner's through its IPC mapping, i.e. NVLink loads and stores).
+qc_status p2p_exchange(qc_state* s, int g, int l) {
+  qc_status st = ensure_peers(s);
+  if (st != QC_OK) return st;
+  const size_t ab = s->dbl ? 16 : 8;
+  int partner;
+  const auto mine = exchange_runs(s->n_loc, s->rank, g, l, &partner);
+  const auto theirs = exchange_runs(s->n_loc, partner, g, l, nullptr);
+  st = pair_barrier(s, partner);  // partner's earlier passes are done with its buffer
+  if (st != QC_OK) return st;
+  const bool lower = s->rank < partner;
+  for (size_t k = 0; k < mine.size(); ++k) {
+    const size_t bytes = mine[k].count * ab, half = (bytes / 2) & ~(size_t)15;
+    const size_t off = lower ? 0 : half, len = lower ? half : bytes - half;
+    char* a = (char*)s->d + mine[k].offset * ab + off;
+    char* b = (char*)s->peers[partner] + theirs[k].offset * ab + off;
+    const int e = launch_swap_regions(a, b, len, s->stream);
+    if (e) return cuda_fail(s, e, "P2P exchange kernel");
+  }
+  return pair_barrier(s, partner);  // the partner's half of the swap is done too
+}
+
+}  // namespace
+
 // Swap physical rank bit g with local bit l (stream-ordered).
 qc_status dist_exchange(qc_state* s, int g, int l) {
   const size_t ab = s->dbl ? 16 : 8;
@@ -196,28 +292,42 @@ qc_status dist_exchange(qc_state* s, int g, int l) {
     }
     return QC_OK;
   }
-  // NCCL: send my runs to the partner, receive its runs into the same places
+  if (s->xmode == 1) return p2p_exchange(s, g, l);
+  // NCCL: send my runs to the partner, receive its runs into the same places.
+  // Chunks alternate between two staging buffers: chunk i's send/recv runs on
+  // the exchange stream while chunk i-1's copy into place runs on the state's
+  // stream (the copy of chunk i waits for its recv; the recv of chunk i+2
+  // into the same buffer waits for that copy).
   Nccl& N = nccl();
   int partner;
   const auto runs = exchange_runs(s->n_loc, s->rank, g, l, &partner);
   const size_t chunk_max = 256ull << 20;
-  if (s->xstage_bytes < chunk_max) {
-    if (s->d_xstage) cudaFree(s->d_xstage);
-    cudaError_t e = cudaMalloc(&s->d_xstage, chunk_max);
-    if (e != cudaSuccess) return fail(QC_ERR_OUT_OF_MEMORY, "exchange staging (%zu B)", chunk_max);
-    s->xstage_bytes = chunk_max;
-  }
+  qc_status st = ensure_xresources(s, 2 * chunk_max);
+  if (st != QC_OK) return st;
+  cudaStream_t xs = s->xstream;
+  cudaEvent_t start = s->xev[0], recv_done[2] = {s->xev[1], s->xev[2]}, copy_done[2] = {s->xev[3], s->xev[4]};
+  cudaError_t e = cudaEventRecord(start, s->stream);  // the exchange follows the state's prior work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(xs, start, 0);
+  if (e != cudaSuccess) return cuda_fail(s, e, "exchange ordering");
+  size_t i = 0;
   for (const auto& run : runs) {
     const size_t bytes = run.count * ab;
     char* base = (char*)s->d + run.offset * ab;
-    for (size_t off = 0; off < bytes; off += chunk_max) {
+    for (size_t off = 0; off < bytes; off += chunk_max, ++i) {
       const size_t m = std::min(chunk_max, bytes - off);
+      const int b = (int)(i & 1);
+      char* stage = (char*)s->d_xstage + b * chunk_max;
+      if (i >= 2 && (e = cudaStreamWaitEvent(xs, copy_done[b], 0)) != cudaSuccess)
+        return cuda_fail(s, e, "exchange ordering");
       int r = N.group_start();
-      if (!r) r = N.send(base + off, m, kNcclUint8, partner, s->nccl_comm, s->stream);
-      if (!r) r = N.recv(s->d_xstage, m, kNcclUint8, partner, s->nccl_comm, s->stream);
+      if (!r) r = N.send(base + off, m, kNcclUint8, partner, s->nccl_comm, xs);
+      if (!r) r = N.recv(stage, m, kNcclUint8, partner, s->nccl_comm, xs);
       const int r2 = N.group_end();
       if (r || r2) return nccl_fail(s, r ? r : r2, "exchange send/recv");
-      cudaError_t e = cudaMemcpyAsync(base + off, s->d_xstage, m, cudaMemcpyDeviceToDevice, s->stream);
+      e = cudaEventRecord(recv_done[b], xs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, recv_done[b], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(base + off, stage, m, cudaMemcpyDeviceToDevice, s->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(copy_done[b], s->stream);
       if (e != cudaSuccess) return cuda_fail(s, e, "exchange copy");
     }
   }
@@ -228,7 +338,9 @@ namespace {
 
 // Build the exchange / segment schedule for an op list from the state's layout.
 // dry_run: schedule only (no device work; segments record their gate count).
-qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPlan* P, bool dry_run = false) {
+// (masks are 64-bit: logical qubits reach 39; a 32-bit shift would alias q and q-32)
+qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPlan* P, const MTable* mt,
+                          bool dry_run = false) {
   const int n = s->n, nl = s->n_loc;
   const int L = nl - 1;  // exchange slot: the top local bit (one contiguous half per direction)
   int lay[64], inv[64];
@@ -238,7 +350,7 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
   std::vector<std::vector<int>> uses(n);
   for (size_t i = 0; i < n_ops; ++i) {
     if (ops[i].op == QC_SWAP && s->relabel) continue;
-    const uint64_t m = nondiag_qubits_mask(ops[i], n);
+    const uint64_t m = op_nondiag_mask(ops[i], mt);
     for (int q = 0; q < n; ++q)
       if (m & (1ull << q)) uses[q].push_back((int)i);
   }
@@ -278,9 +390,13 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       P->relabels++;
       continue;
     }
-    const uint64_t nd = nondiag_qubits_mask(op, n);
+    const uint64_t nd = op_nondiag_mask(op, mt);
     uint64_t op_qubits = 0;
-    for (int t = 0; t < kArity[op.op]; ++t) op_qubits |= 1ull << op.qubits[t];
+    {
+      int qs[QC_MGATE_MAX_QUBITS];
+      const int nq = qc::op_qubits(op, mt, qs);
+      for (int t = 0; t < nq; ++t) op_qubits |= 1ull << qs[t];
+    }
     for (int q = 0; q < n; ++q) {
       if (!(nd & (1ull << q)) || lay[q] < nl) continue;
       // qubit q is non-diagonal and global: bring it to local bit L
@@ -322,7 +438,7 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       inv[lay[qg]] = qg;
       inv[lay[ql]] = ql;
     }
-    PGate pg = lower(op, lay);
+    PGate pg = lower(op, lay, mt);
     seg.push_back(pg);
   }
   qc_status r = flush();
@@ -358,7 +474,7 @@ qc_status enqueue_dist(qc_state* s, DistPlan* P) {
 
 // Host-only schedule for tests (qc_debug.h): steps as (kind, g, l, gates).
 qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
-                            std::vector<int>& out, std::vector<int>& layout_out) {
+                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt) {
   qc_state s;
   s.n = n;
   s.world = world;
@@ -367,7 +483,7 @@ qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, s
   s.dist = 1;
   for (int q = 0; q < n; ++q) s.layout[q] = n - 1 - q;
   DistPlan P;
-  const qc_status r = build_dist_plan(&s, ops, n_ops, &P, true);
+  const qc_status r = build_dist_plan(&s, ops, n_ops, &P, mt, true);
   if (r != QC_OK) return r;
   for (auto& st : P.steps) {
     out.push_back(st.kind);
@@ -379,7 +495,7 @@ qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, s
   return QC_OK;
 }
 
-qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops) {
+qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* mt) {
   {
     const qc_status c = ensure_fused_configured(s);
     if (c != QC_OK) return c;
@@ -388,20 +504,23 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops) {
                         ((uint64_t)s->tile_bits << 8) ^ ((uint64_t)s->row_bits << 16) ^
                         ((uint64_t)s->tma_mode << 24) ^ ((uint64_t)s->jit << 28) ^ ((uint64_t)s->remap << 32) ^
                         ((uint64_t)s->ctas << 36) ^ ((uint64_t)s->fusion << 56);
-  const uint64_t key = hash_ops(ops, n_ops, s->layout, s->n, salt);
+  std::vector<uint8_t> mkey = mtable_key(ops, n_ops, mt);
+  uint64_t key = hash_ops(ops, n_ops, s->layout, s->n, salt);
+  for (uint8_t b : mkey) key = (key ^ b) * 0x100000001b3ull;
   DistPlan* P = nullptr;
   if (!s->dcache) s->dcache = new DistCache();
   auto& dplans = s->dcache->plans;
   auto it = dplans.find(key);
   if (it != dplans.end() && it->second->ops.size() == n_ops &&
-      std::memcmp(it->second->ops.data(), ops, n_ops * sizeof(qc_gate)) == 0 &&
+      std::memcmp(it->second->ops.data(), ops, n_ops * sizeof(qc_gate)) == 0 && it->second->mkey == mkey &&
       std::memcmp(it->second->layout_in.data(), s->layout, sizeof(int) * s->n) == 0) {
     P = it->second.get();
   } else {
     auto np = std::make_unique<DistPlan>();
     np->ops.assign(ops, ops + n_ops);
+    np->mkey = std::move(mkey);
     np->layout_in.assign(s->layout, s->layout + s->n);
-    const qc_status r = build_dist_plan(s, ops, n_ops, np.get());
+    const qc_status r = build_dist_plan(s, ops, n_ops, np.get(), mt);
     if (r != QC_OK) return r;
     P = np.get();
     if (dplans.size() > 32) dplans.clear();

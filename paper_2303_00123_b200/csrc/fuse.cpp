@@ -26,11 +26,18 @@ bool pgate_is_two(const PGate& g) {
          g.kind == GK::PERM2 || g.kind == GK::DIAG2;
 }
 
-uint64_t pgate_bits(const PGate& g) {
-  uint64_t m = g.cmask | (1ull << g.t0);
+uint64_t pgate_targets(const PGate& g) {
+  if (g.kind == GK::DENSEK) {
+    uint64_t m = 0;
+    for (int j = 0; j < g.nt; ++j) m |= 1ull << g.tk[j];
+    return m;
+  }
+  uint64_t m = 1ull << g.t0;
   if (pgate_is_two(g)) m |= 1ull << g.t1;
   return m;
 }
+
+uint64_t pgate_bits(const PGate& g) { return g.cmask | pgate_targets(g); }
 
 void pgate_dense4(const PGate& g, cd out[16]) {
   for (int i = 0; i < 16; ++i) out[i] = 0;

@@ -300,6 +300,33 @@ __device__ __forceinline__ void qc_m2_dense(C (&v)[kSlots], const C* __restrict_
   }
 }
 
+// F_MK (generic 3- / 4-target gate) in canonical slot order: MISS = the slot
+// bit not in the op (k = 3) or 4 (k = 4: every slot bit, index = slot).  A
+// slot-bit predicate can only be on MISS.
+template <int MISS>
+__device__ __forceinline__ constexpr int qc_mk_expand(int c) {
+  return MISS >= 4 ? c : (((c >> MISS) << (MISS + 1)) | (c & ((1 << MISS) - 1)));
+}
+template <int MISS, typename C>
+__device__ __forceinline__ void qc_mk_dense(C (&v)[kSlots], const C* __restrict__ cp, uint32_t sm, uint32_t sv) {
+  constexpr int K = MISS < 4 ? 3 : 4, D = 1 << K, NB = MISS < 4 ? 2 : 1;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int s0 = MISS < 4 ? (b << MISS) : 0;
+    if ((s0 & sm) != sv) continue;
+    C a[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) a[c] = v[s0 | qc_mk_expand<MISS>(c)];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      C o = qc_cmul(cp[D * r], a[0]);
+#pragma unroll
+      for (int c = 1; c < D; ++c) qc_cmac(o, cp[D * r + c], a[c]);
+      v[s0 | qc_mk_expand<MISS>(r)] = o;
+    }
+  }
+}
+
 template <typename C>
 __device__ __forceinline__ void qc_scale_slots(C (&v)[kSlots], const C w, uint32_t sm, uint32_t sv) {
 #pragma unroll

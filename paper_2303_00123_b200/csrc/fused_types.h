@@ -38,7 +38,9 @@ constexpr int kPadBytes = 16;         // smem padding per row (bank-conflict rel
 constexpr int kMaxPrun = 64;          // phase runs with a per-tile factor, per pass
 
 // Fused op kinds, bit sources and exact matrix patterns.
-enum FKind : uint8_t { F_M1 = 0, F_M2 = 1, F_DSCALE = 2, F_PRUN = 3 };
+// F_MK: dense 2^k x 2^k (k = 3, 4) on k slot bits in canonical order; sb1 = k,
+// sb0 = the slot bit NOT in the op when k = 3.
+enum FKind : uint8_t { F_M1 = 0, F_M2 = 1, F_DSCALE = 2, F_PRUN = 3, F_MK = 4 };
 enum FSrc : uint8_t { S_SLOT = 0, S_LOCAL = 1, S_OUTER = 2, S_NONE = 3 };
 enum FPat : uint8_t { P_DENSE = 0, P_DIAG = 1, P_ANTI = 2, P_MOVE = 3, P_PAIRS1 = 4, P_PAIRS2 = 5,
                       P_PAIRS3 = 6 };

@@ -137,6 +137,17 @@ struct InterpBody {
 #undef QC_M2_CASE
         break;
       }
+      case F_MK: {
+        const int miss = h.sb1 == 4 ? 4 : h.sb0;
+        switch (miss) {
+          case 0: qc_mk_dense<0>(v, cp, sm, sv); break;
+          case 1: qc_mk_dense<1>(v, cp, sm, sv); break;
+          case 2: qc_mk_dense<2>(v, cp, sm, sv); break;
+          case 3: qc_mk_dense<3>(v, cp, sm, sv); break;
+          default: qc_mk_dense<4>(v, cp, sm, sv); break;
+        }
+        break;
+      }
       case F_DSCALE: {
         const int bit = (h.dsrc == S_LOCAL) ? (int)((lb >> h.dbit) & 1u) : (int)((tbase >> h.dbit) & 1ull);
         if (bit == 0 && (h.flags & 1)) break;

@@ -41,6 +41,7 @@ struct Item {
 #pragma unroll 4
     for (int i = 0; i < 4; ++i)
       if (i < a.nins) x = insert0(x, a.ins[i]);
+    for (int i = 4; i < a.nins; ++i) x = insert0(x, a.ins[i]);  // many controls (qc_mgate)
     x |= a.setmask;
     if (KIND == (int)GK::DENSE1 || KIND == (int)GK::PERM1) {
       id[0] = x;
@@ -126,8 +127,81 @@ __global__ void __launch_bounds__(256) gate_kernel(typename CT<T>::type* __restr
   }
 }
 
+// Generic gate on K = 3..4 targets: one thread per group of 2^K amplitudes
+// (zero bits inserted at the sorted target + control positions, control
+// values OR-ed in), 2^K x 2^K complex matvec with the matrix read
+// from parameter space (uniform operands), loads of a group before its stores.
+template <typename T, int K>
+__global__ void __launch_bounds__(128) gate_kernel_k(typename CT<T>::type* __restrict__ s,
+                                                     const __grid_constant__ GateArgsK<T> a) {
+  using C = typename CT<T>::type;
+  constexpr int D = 1 << K;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.count; j += stride) {
+    uint64_t x = j;
+    for (int i = 0; i < a.nins; ++i) x = insert0(x, a.ins[i]);
+    x |= a.setmask;
+    uint64_t id[D];
+    C v[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      uint64_t y = x;
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+        if ((c >> (K - 1 - t)) & 1) y |= 1ull << a.tpos[t];
+      id[c] = y;
+      v[c] = s[y];
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      T ore = 0, oim = 0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const T mr = a.m[2 * (D * r + c)], mi = a.m[2 * (D * r + c) + 1];
+        ore = fma(mr, v[c].x, ore);
+        ore = fma(-mi, v[c].y, ore);
+        oim = fma(mr, v[c].y, oim);
+        oim = fma(mi, v[c].x, oim);
+      }
+      C o;
+      o.x = ore;
+      o.y = oim;
+      s[id[r]] = o;
+    }
+  }
+}
+
+template <typename T>
+int launch_gate_k(void* state, int n, const PGate& g, cudaStream_t st) {
+  GateArgsK<T> a{};
+  const uint64_t ins = g.cmask | pgate_targets(g);
+  a.nins = 0;
+  for (int p = 0; p < n; ++p)
+    if (ins & (1ull << p)) a.ins[a.nins++] = p;
+  a.count = 1ull << (n - a.nins);
+  a.setmask = g.cval;
+  a.k = g.nt;
+  for (int t = 0; t < g.nt; ++t) a.tpos[t] = g.tk[t];
+  const size_t d2 = (size_t)1 << (2 * g.nt);
+  for (size_t i = 0; i < d2; ++i) {
+    a.m[2 * i] = (T)(*g.mk)[i].real();
+    a.m[2 * i + 1] = (T)(*g.mk)[i].imag();
+  }
+  using C = typename CT<T>::type;
+  C* s = reinterpret_cast<C*>(state);
+  const int threads = 128;
+  uint64_t blocks = (a.count + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (g.nt == 3) gate_kernel_k<T, 3><<<(unsigned)blocks, threads, 0, st>>>(s, a);
+  else gate_kernel_k<T, 4><<<(unsigned)blocks, threads, 0, st>>>(s, a);
+  return (int)cudaGetLastError();
+}
+
 template <typename T>
 int launch_gate_t(void* state, int n, const PGate& g, cudaStream_t st) {
+  if (g.kind == GK::DENSEK) return launch_gate_k<T>(state, n, g, st);
   GateArgs<T> a{};
   uint64_t ins = g.cmask;
   int nt = 0;

@@ -57,9 +57,26 @@ __global__ void init_random_kernel<float2>(float2* s, uint64_t N, uint64_t first
 }
 
 // Swap two equal, disjoint device ranges (loopback exchange), 16-byte units.
+// Swap two equal regions (16-B words).  4 words of each region per thread in
+// flight (all 8 loads before the stores): the exchange's peer region is read
+// and written over NVLink, whose latency needs the extra bytes in flight.
 __global__ void swap_regions_kernel(uint4* __restrict__ a, uint4* __restrict__ b, uint64_t n16) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n16; j += stride) {
+  uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; j + 3 * stride < n16; j += 4 * stride) {
+    uint4 x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = a[j + u * stride];
+      y[u] = b[j + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[j + u * stride] = y[u];
+      b[j + u * stride] = x[u];
+    }
+  }
+  for (; j < n16; j += stride) {
     const uint4 x = a[j], y = b[j];
     a[j] = y;
     b[j] = x;
@@ -137,7 +154,10 @@ int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream
 int launch_swap_regions(void* a, void* b, uint64_t bytes, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const uint64_t n16 = bytes / 16;
-  swap_regions_kernel<<<blocks_for(n16, 256), 256, 0, st>>>((uint4*)a, (uint4*)b, n16);
+  const uint64_t cap = (uint64_t)sm_count() * 8;  // 8 x 256 threads per SM, grid-stride
+  uint64_t blocks = blocks_for((n16 + 3) / 4, 256);
+  if (blocks > cap) blocks = cap;
+  swap_regions_kernel<<<(unsigned)blocks, 256, 0, st>>>((uint4*)a, (uint4*)b, n16);
   return (int)cudaGetLastError();
 }
 

@@ -28,11 +28,7 @@ namespace {
 
 inline int popc(uint64_t x) { return std::popcount(x); }
 
-uint64_t target_mask(const PGate& g) {
-  uint64_t m = 1ull << g.t0;
-  if (pgate_is_two(g)) m |= 1ull << g.t1;
-  return m;
-}
+uint64_t target_mask(const PGate& g) { return pgate_targets(g); }
 uint64_t need_mask(const PGate& g) { return g.kind == GK::DIAG1 ? 0ull : target_mask(g); }
 
 // Algorithmic flops per state amplitude of one (block-fused) gate inside a
@@ -46,12 +42,14 @@ double gate_flops(const PGate& g) {
     case GK::DENSE2: return 30 * ctrl;
     case GK::SPARSE2: return 14 * ctrl;
     case GK::DIAG2: return 6 * ctrl;
+    case GK::DENSEK: return (6.0 + 8.0 * ((1 << g.nt) - 1)) * ctrl;
     default: return 0;  // permutations / swaps: register moves
   }
 }
 
 size_t blob_estimate(const PGate& g) {
   if (g.kind == GK::DIAG1) return 48;
+  if (g.kind == GK::DENSEK) return 48 + ((size_t)16 << (2 * g.nt));
   if (pgate_is_two(g)) return 48 + 16 * 16;
   return 48 + 4 * 16;
 }
@@ -167,8 +165,46 @@ void rows_to_ir(const cd* M, int dim, FOpIR& o) {
   for (int i = 0; i < 16; ++i) o.coefs.push_back(M[i]);
 }
 
+// Generic k-target gate (k = 3, 4) -> F_MK in canonical slot order: the
+// listed targets' slot bits s_j; matrix index bit i of the canonical form is
+// the i-th lowest of {s_j}, so M'[perm(r)][perm(c)] = M[r][c] (a relabelling
+// of the same operator's index bits).
+FOpIR convert_mk(const PGate& g, const Ctx& c) {
+  FOpIR o;
+  set_pred(o.h, g, c);
+  o.h.kind = F_MK;
+  const int k = g.nt, d = 1 << k;
+  int sl[4], rank[4];
+  unsigned present = 0;
+  for (int j = 0; j < k; ++j) {
+    sl[j] = c.slot(g.tk[j]);
+    present |= 1u << sl[j];
+  }
+  for (int j = 0; j < k; ++j) {  // rank of s_j among the op's slot bits (0 = lowest)
+    rank[j] = 0;
+    for (int i = 0; i < k; ++i) rank[j] += sl[i] < sl[j];
+  }
+  o.h.sb1 = (uint8_t)k;
+  o.h.sb0 = 0;
+  if (k == 3)
+    for (int b = 0; b < kSlotBits; ++b)
+      if (!(present & (1u << b))) o.h.sb0 = (uint8_t)b;
+  auto perm = [&](int r) {  // listed index (target j = bit k-1-j) -> canonical index
+    int x = 0;
+    for (int j = 0; j < k; ++j)
+      if ((r >> (k - 1 - j)) & 1) x |= 1 << rank[j];
+    return x;
+  };
+  o.mk.assign((size_t)d * d, cd(0));
+  for (int r = 0; r < d; ++r)
+    for (int cc = 0; cc < d; ++cc) o.mk[(size_t)perm(r) * d + perm(cc)] = (*g.mk)[(size_t)r * d + cc];
+  o.coefs = o.mk;
+  return o;
+}
+
 // A single (non-run) gate -> one fused op.
 FOpIR convert(const PGate& g, const Ctx& c) {
+  if (g.kind == GK::DENSEK) return convert_mk(g, c);
   FOpIR o;
   set_pred(o.h, g, c);
   if (pgate_is_two(g)) {
@@ -354,6 +390,7 @@ void swap_bits(PGate& g, int a, int b) {
   auto mv = [&](int p) { return p == a ? b : (p == b ? a : p); };
   g.t0 = mv(g.t0);
   if (pgate_is_two(g)) g.t1 = mv(g.t1);
+  for (int j = 0; j < g.nt; ++j) g.tk[j] = mv(g.tk[j]);
   auto mvmask = [&](uint64_t m) {
     const uint64_t ba = (m >> a) & 1ull, bb = (m >> b) & 1ull;
     m &= ~((1ull << a) | (1ull << b));
@@ -835,6 +872,19 @@ double pass_flops_per_amp(const FusedPassPlan& pp) {
             first = false;
           }
           if (!ident) f += fr;
+        }
+        total += f / dim * pred;
+      } else if (h.kind == F_MK) {
+        const int dim = 1 << h.sb1;
+        double f = 0;
+        for (int r = 0; r < dim; ++r) {
+          bool first = true;
+          for (int cc = 0; cc < dim; ++cc) {
+            const cd z = o.mk[(size_t)r * dim + cc];
+            if (is0(z)) continue;
+            f += first ? (unit(z) ? 0 : 6) : (unit(z) ? 2 : 8);
+            first = false;
+          }
         }
         total += f / dim * pred;
       } else if (h.kind == F_DSCALE) {

@@ -16,6 +16,7 @@
 #pragma once
 #include <complex>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -34,7 +35,8 @@ enum class GK : int32_t {
   DENSE1 = 0, PERM1 = 1, DIAG1 = 2, DENSE2 = 3, SWAP2 = 4,
   SPARSE2 = 5,  // 4x4, <= 2 non-zeros per row: out[r] = m[2r] x[col[2r]] + m[2r+1] x[col[2r+1]]
   PERM2 = 6,    // 4x4 permutation: out[r] = x[col[r]]
-  DIAG2 = 7     // diag(m[0..3])
+  DIAG2 = 7,    // diag(m[0..3])
+  DENSEK = 8    // generic gate (qc_mgate): 2^nt x 2^nt dense on targets tk[0..nt) (tk[0] = MSB), nt = 3..4
 };
 
 struct PGate {
@@ -45,7 +47,12 @@ struct PGate {
   int8_t col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   bool d0_is_one = false;        // DIAG1 with d0 == 1 exactly: only the |1> half changes
   int src_op = -1;
+  int nt = 0;                    // DENSEK: target count and physical target bits (MSB first)
+  int tk[4] = {-1, -1, -1, -1};
+  std::shared_ptr<const std::vector<cd>> mk;  // DENSEK: row-major 2^nt x 2^nt
 };
+
+uint64_t pgate_targets(const PGate& g);         // physical target bits
 
 bool pgate_is_two(const PGate& g);
 uint64_t pgate_bits(const PGate& g);            // targets | controls
@@ -71,6 +78,8 @@ struct FOpIR {
   std::vector<Term> sterms;
   bool folded = false;
   cd dense[16];              // M1/M2: the exact matrix (row-major), for code generation
+  std::vector<cd> mk;        // F_MK: 2^k x 2^k over the op's slot bits in canonical order
+                             // (matrix index bit j = the j-th lowest of its slot bits)
 };
 
 struct FusedPassPlan {
@@ -104,13 +113,26 @@ std::vector<uint8_t> pack_plan(FusedPlan& plan, bool dbl);
 template <typename T>
 struct GateArgs {
   uint64_t count;         // work items
-  int32_t nins;           // zero-bit insertions (ascending positions)
-  int32_t ins[4];
+  int32_t nins;           // zero-bit insertions (ascending positions): targets + controls
+  int32_t ins[QC_MGATE_MAX_QUBITS];
   uint64_t setmask;       // OR'ed after insertion (control values)
   int32_t t0, t1;
   int32_t d0_is_one;
   int32_t pad;
   T m[32];
+};
+
+// Per-gate kernel of a generic gate on k = 3..4 targets (qc_mgate): the
+// matrix travels in the kernel's parameter space (__grid_constant__).
+template <typename T>
+struct GateArgsK {
+  uint64_t count;         // groups of 2^k amplitudes
+  int32_t nins;
+  int32_t ins[QC_MGATE_MAX_QUBITS];
+  uint64_t setmask;       // control values
+  int32_t k;
+  int32_t tpos[4];        // physical target bits, tpos[0] = matrix MSB
+  T m[2 * 256];           // row-major 2^k x 2^k, interleaved re,im
 };
 
 // NVRTC-specialised fused passes (jit.cu).

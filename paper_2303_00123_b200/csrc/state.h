@@ -14,6 +14,7 @@ namespace qc {
 
 struct PlanEntry {
   std::vector<qc_gate> ops;          // exact copy (collision check)
+  std::vector<uint8_t> mkey;         // referenced generic gates' contents (collision check)
   std::vector<int> layout_in, layout_out;
   std::vector<PassDesc> passes;
   void* d_blob = nullptr;
@@ -39,14 +40,29 @@ struct PlanEntry {
 };
 
 
+// Generic gates of qc_run_circuit_ex / qc_apply_mgate, copied (matrix
+// included) so plans never point into caller memory.
+struct MGate {
+  int n_ctrl = 0, n_targ = 0;
+  int qubits[QC_MGATE_MAX_QUBITS] = {};
+  uint32_t ctrl_state = 0;
+  std::vector<cd> m;  // row-major 2^n_targ x 2^n_targ
+};
+using MTable = std::vector<MGate>;
+// Content bytes of the gates an op list references (plan-cache key / check).
+std::vector<uint8_t> mtable_key(const qc_gate* ops, size_t n_ops, const MTable* mt);
+// Logical qubits of an op (controls first), and its non-diagonal targets.
+int op_qubits(const qc_gate& g, const MTable* mt, int* out);
+uint64_t op_nondiag_mask(const qc_gate& g, const MTable* mt);
+
 struct DistPlan;   // dist.cu
 struct DistCache;  // dist.cu
 
 // api.cu helpers shared with dist.cu
 qc_status fail(qc_status st, const char* fmt, ...);
 qc_status cuda_fail(qc_state* s, int e, const char* what);
-PGate lower(const qc_gate& g, const int* layout);
-qc_status validate_gate(int n, const qc_gate& g, size_t idx);
+PGate lower(const qc_gate& g, const int* layout, const MTable* mt = nullptr);
+qc_status validate_gate(int n, const qc_gate& g, size_t idx, const MTable* mt = nullptr);
 uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt);
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
                             PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0, bool remap = false);
@@ -58,7 +74,7 @@ extern const int kArity[16];
 extern const int kNctrl[16];
 
 // dist.cu
-qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops);
+qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* mt = nullptr);
 qc_status dist_canonicalize(qc_state* s);
 qc_status dist_exchange(qc_state* s, int g, int l);
 qc_status nccl_create_comm(qc_state* s, const void* unique_id);
@@ -67,7 +83,7 @@ qc_status nccl_allreduce_sum(qc_state* s, double* host_value);
 void nccl_destroy(qc_state* s);
 void dist_release(qc_state* s);  // drop sharded plans + communicator
 qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
-                            std::vector<int>& out, std::vector<int>& layout_out);
+                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt = nullptr);
 struct ExchangeRun {
   uint64_t offset;  // amplitudes, within the shard
   uint64_t count;
@@ -111,8 +127,13 @@ struct qc_state {
   int dist = 0;       // 0: single GPU; 1: loopback (all ranks' shards in this buffer); 2: NCCL
   int world = 1, rank = 0, n_loc = 0;
   void* nccl_comm = nullptr;
-  void* d_xstage = nullptr;
+  void* d_xstage = nullptr;          // exchange staging: two chunks (ping-pong)
   size_t xstage_bytes = 0;
+  int xmode = 0;                     // QC_OPT_EXCHANGE: 0 NCCL send/recv, 1 P2P swap kernel
+  cudaStream_t xstream = nullptr;    // NCCL exchange stream (copies stay on `stream`)
+  cudaEvent_t xev[5] = {};           // start, recv_done[2], copy_done[2]
+  std::vector<void*> peers;          // P2P: every rank's state buffer, IPC-mapped (own: d)
+  int* d_token = nullptr;            // P2P: pairwise barrier token (2 ints)
   int64_t last_exchanges = 0;
   qc::DistCache* dcache = nullptr;  // sharded plans (owned by dist.cu)
   ~qc_state();

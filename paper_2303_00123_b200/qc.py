@@ -29,15 +29,29 @@ ARITY = {"H": 1, "X": 1, "Y": 1, "Z": 1, "P": 1, "RX": 1, "RY": 1, "RZ": 1, "CNO
 QC_CTRL_ONES = 0xFFFFFFFF
 OPTIONS = {"fusion": 0, "relabel_swap": 1, "use_graph": 2, "tile_bits": 3, "ctas": 4,
            "block_fusion": 5, "jit": 6, "row_bits": 7,
-           "tma_mode": 8, "remap": 9}
+           "tma_mode": 8, "remap": 9, "exchange": 10}
 
 GATE_DTYPE = np.dtype([("op", "<i4"), ("qubits", "<i4", (3,)), ("ctrl_state", "<u4"),
                        ("flags", "<u4"), ("theta", "<f8"), ("m", "<f8", (32,))])
 assert GATE_DTYPE.itemsize == 288
+QC_MGATE = 16
+MGATE_DTYPE = np.dtype([("n_ctrl", "<i4"), ("n_targ", "<i4"), ("qubits", "<i4", (16,)),
+                        ("ctrl_state", "<u4"), ("flags", "<u4"), ("matrix", "<u8")])
+assert MGATE_DTYPE.itemsize == 88
+
+
+class GateArray(np.ndarray):
+    """qc_gate records plus the qc_mgate table their QC_MGATE ops refer to
+    (``mtab``; ``keep`` holds the matrices the table points into)."""
+
+    def __array_finalize__(self, obj):
+        self.mtab = getattr(obj, "mtab", None)
+        self.keep = getattr(obj, "keep", None)
 
 EXPORTS = ["qc_state_create", "qc_state_create_ex", "qc_state_wrap", "qc_state_destroy",
            "qc_state_create_dist", "qc_state_create_loopback", "qc_nccl_unique_id",
            "qc_state_init_basis", "qc_state_init_random", "qc_apply_gate", "qc_run_circuit",
+           "qc_run_circuit_ex", "qc_apply_mgate",
            "qc_state_read", "qc_state_write", "qc_state_canonicalize", "qc_state_sync",
            "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_qasm_parse", "qc_qasm_emit",
            "qc_last_error", "qc_version"]
@@ -97,6 +111,8 @@ def lib() -> ctypes.CDLL:
     L.qc_state_init_random.argtypes = [vp, u64]
     L.qc_apply_gate.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
     L.qc_run_circuit.argtypes = [vp, vp, sz]
+    L.qc_run_circuit_ex.argtypes = [vp, vp, sz, vp, sz]
+    L.qc_apply_mgate.argtypes = [vp, vp]
     L.qc_state_read.argtypes = [vp, u64, u64, vp]
     L.qc_state_write.argtypes = [vp, u64, u64, vp]
     L.qc_state_canonicalize.argtypes = [vp]
@@ -138,13 +154,34 @@ def _check(rc: int):
         raise QCError(rc, lib().qc_last_error().decode())
 
 
+def encode_mgate(op, keep: list) -> np.ndarray:
+    """A generic ("MCU") gate record -> one qc_mgate struct (matrix kept alive in ``keep``)."""
+    g = np.zeros(1, dtype=MGATE_DTYPE)
+    nc = int(op.nctrl)
+    g[0]["n_ctrl"] = nc
+    g[0]["n_targ"] = len(op.qubits) - nc
+    g[0]["qubits"] = list(op.qubits) + [0] * (16 - len(op.qubits))
+    g[0]["ctrl_state"] = op.ctrl_state
+    m = np.ascontiguousarray(np.asarray(op.matrix, dtype=np.complex128)).view(np.float64).reshape(-1)
+    keep.append(m)
+    g[0]["matrix"] = m.ctypes.data
+    return g
+
+
 def encode_ops(ops: Iterable) -> np.ndarray:
     """Gate records (objects with name, qubits, theta, matrix, ctrl_state) ->
-    contiguous array of ``qc_gate`` structs."""
+    contiguous array of ``qc_gate`` structs (a :class:`GateArray` carrying the
+    qc_mgate table when the list holds generic "MCU" gates)."""
     ops = list(ops)
     arr = np.zeros(len(ops), dtype=GATE_DTYPE)
+    mt, keep = [], []
     for i, op in enumerate(ops):
         name = op.name
+        if name == "MCU":
+            arr[i]["op"] = QC_MGATE
+            arr[i]["qubits"] = [len(mt), 0, 0]
+            mt.append(encode_mgate(op, keep))
+            continue
         arr[i]["op"] = OPS[name]
         q = list(op.qubits) + [0] * (3 - len(op.qubits))
         arr[i]["qubits"] = q
@@ -159,6 +196,10 @@ def encode_ops(ops: Iterable) -> np.ndarray:
             flat[0:2 * m.size:2] = m.real
             flat[1:2 * m.size:2] = m.imag
             arr[i]["m"] = flat
+    if mt:
+        arr = arr.view(GateArray)
+        arr.mtab = np.concatenate(mt)
+        arr.keep = keep
     return arr
 
 
@@ -263,8 +304,22 @@ class State:
 
     def run(self, ops) -> None:
         arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
+        mt = getattr(arr, "mtab", None)
         arr = np.ascontiguousarray(arr)
-        _check(lib().qc_run_circuit(self._h, arr.ctypes.data if len(arr) else None, len(arr)))
+        if mt is None:
+            _check(lib().qc_run_circuit(self._h, arr.ctypes.data if len(arr) else None, len(arr)))
+        else:
+            _check(lib().qc_run_circuit_ex(self._h, arr.ctypes.data if len(arr) else None, len(arr),
+                                           mt.ctypes.data, len(mt)))
+
+    def apply_mgate(self, qubits: Sequence[int], matrix, n_ctrl: int = 0, ctrl_state: Optional[int] = None):
+        """One generic gate (controls first in ``qubits``) via qc_apply_mgate."""
+        import types
+        op = types.SimpleNamespace(qubits=tuple(qubits), nctrl=n_ctrl, matrix=matrix,
+                                   ctrl_state=(1 << n_ctrl) - 1 if ctrl_state is None else ctrl_state)
+        keep = []
+        g = encode_mgate(op, keep)
+        _check(lib().qc_apply_mgate(self._h, g.ctypes.data))
 
     # -- I/O
     def read(self, first: int = 0, count: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:

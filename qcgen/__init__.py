@@ -26,7 +26,8 @@ import numpy as np
 __all__ = [
     "GOLDEN", "splitmix64", "u_pm1", "random_state", "random_state_even_parity",
     "angles", "Op", "ARITY", "NCTRL", "qft", "tfxy", "inverse", "random_circuit",
-    "random_unitary", "gate_counts", "STATE_SEED", "ANGLE_SEED",
+    "random_unitary", "gate_counts", "STATE_SEED", "ANGLE_SEED", "random_mcu_circuit",
+    "MCU_MAX_QUBITS", "MCU_MAX_TARGETS",
 ]
 
 STATE_SEED = 12345
@@ -117,6 +118,13 @@ THETA_OPS = {"P", "RX", "RY", "RZ", "CP"}
 MATRIX_DIM = {"U1": 2, "CU1": 2, "U2": 4}
 
 
+# "MCU": the generic gate of SURVEY 8(f) rows 1-2 -- ``nctrl``
+# controls listed first, then k = len(qubits) - nctrl targets carrying a dense
+# 2^k x 2^k ``matrix`` (big-endian over the listed targets, eq:kron).
+MCU_MAX_QUBITS = 16
+MCU_MAX_TARGETS = 4
+
+
 @dataclass
 class Op:
     """One gate application.  ``qubits`` lists controls first."""
@@ -125,9 +133,24 @@ class Op:
     theta: Optional[float] = None
     matrix: Optional[np.ndarray] = None
     ctrl_state: Optional[int] = None  # bit t = required state of control t
+    nctrl: Optional[int] = None       # MCU only: number of leading control qubits
 
     def __post_init__(self):
         self.qubits = tuple(int(q) for q in self.qubits)
+        if self.name == "MCU":
+            nq = len(self.qubits)
+            if self.nctrl is None or not (0 <= self.nctrl < nq <= MCU_MAX_QUBITS):
+                raise ValueError("MCU needs 0 <= nctrl < len(qubits) <= 16")
+            k = nq - self.nctrl
+            if k > MCU_MAX_TARGETS:
+                raise ValueError("MCU takes at most 4 target qubits")
+            m = np.asarray(self.matrix, dtype=np.complex128)
+            if m.shape != (1 << k, 1 << k):
+                raise ValueError(f"MCU with {k} targets needs a {1 << k}x{1 << k} matrix")
+            self.matrix = m
+            if self.ctrl_state is None:
+                self.ctrl_state = (1 << self.nctrl) - 1
+            return
         if self.name not in ARITY:
             raise ValueError(f"unknown op {self.name}")
         if len(self.qubits) != ARITY[self.name]:
@@ -232,9 +255,9 @@ def inverse(ops: Sequence[Op]) -> List[Op]:
     for op in reversed(ops):
         if op.name in THETA_OPS:
             out.append(Op(op.name, op.qubits, theta=-op.theta, ctrl_state=op.ctrl_state))
-        elif op.name in MATRIX_DIM:
+        elif op.name in MATRIX_DIM or op.name == "MCU":
             out.append(Op(op.name, op.qubits, matrix=op.matrix.conj().T.copy(),
-                          ctrl_state=op.ctrl_state))
+                          ctrl_state=op.ctrl_state, nctrl=op.nctrl))
         else:  # H X Y Z CNOT CZ SWAP CCX are self-inverse
             out.append(Op(op.name, op.qubits, ctrl_state=op.ctrl_state))
     return out
@@ -267,6 +290,31 @@ def random_circuit(n: int, n_gates: int, seed: int = 1,
         th = float(rng.uniform(-2 * math.pi, 2 * math.pi)) if name in THETA_OPS else None
         m = random_unitary(MATRIX_DIM[name], rng) if name in MATRIX_DIM else None
         ops.append(Op(name, qs, theta=th, matrix=m, ctrl_state=cs))
+    return ops
+
+
+def random_mcu_circuit(n: int, n_gates: int, seed: int = 1, max_ctrl: int = 4, max_targ: int = 4,
+                       mix: Sequence[str] = ALL_KINDS, p_mcu: float = 0.5,
+                       perm_frac: float = 0.0) -> List[Op]:
+    """Random circuit mixing generic MCU gates (random control count
+    0..max_ctrl, target count 1..max_targ, random ctrl_state, Haar-ish matrix;
+    with probability perm_frac a random permutation matrix -- a pure move)
+    with the named kinds of ``mix``."""
+    rng = np.random.default_rng(seed)
+    named = random_circuit(n, n_gates, seed=seed + 7919, kinds=mix)
+    ops = []
+    for i in range(n_gates):
+        if rng.random() >= p_mcu:
+            ops.append(named[i])
+            continue
+        k = int(rng.integers(1, min(max_targ, n) + 1))
+        c = int(rng.integers(0, min(max_ctrl, n - k) + 1))
+        qs = tuple(int(q) for q in rng.choice(n, size=k + c, replace=False))
+        if rng.random() < perm_frac:
+            m = np.eye(1 << k, dtype=np.complex128)[rng.permutation(1 << k)]
+        else:
+            m = random_unitary(1 << k, rng)
+        ops.append(Op("MCU", qs, matrix=m, nctrl=c, ctrl_state=int(rng.integers(1 << c))))
     return ops
 
 

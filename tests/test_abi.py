@@ -52,8 +52,9 @@ def test_gate_struct_layout_matches_header():
 #include <stddef.h>
 #include "qc_debug.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu\n", sizeof(qc_gate), sizeof(qc_info), offsetof(qc_info, last_flops_per_amp),
-         sizeof(qc_plan_stats), offsetof(qc_plan_stats, flops_per_amp));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(qc_gate), sizeof(qc_info), offsetof(qc_info, last_flops_per_amp),
+         sizeof(qc_plan_stats), offsetof(qc_plan_stats, flops_per_amp), sizeof(qc_mgate),
+         offsetof(qc_mgate, ctrl_state), offsetof(qc_mgate, matrix));
   return 0;
 }
 """
@@ -65,12 +66,34 @@ int main(void) {
     assert sz[0] == qc.GATE_DTYPE.itemsize
     assert sz[1] == ctypes.sizeof(qc.qc_info) and sz[2] == qc.qc_info.last_flops_per_amp.offset
     assert sz[3] == ctypes.sizeof(qc.qc_plan_stats) and sz[4] == qc.qc_plan_stats.flops_per_amp.offset
+    assert sz[5] == qc.MGATE_DTYPE.itemsize
+    assert sz[6] == qc.MGATE_DTYPE.fields["ctrl_state"][1] and sz[7] == qc.MGATE_DTYPE.fields["matrix"][1]
 
 
 def test_op_codes_match_header():
     txt = open(os.path.join(ROOT, "include", "qc.h")).read()
     for name, code in qc.OPS.items():
         assert re.search(rf"QC_{name}\s*=\s*{code}\b", txt), name
+    assert re.search(rf"QC_MGATE\s*=\s*{qc.QC_MGATE}\b", txt)
+
+
+def test_encode_generic_gates():
+    """MCU records -> QC_MGATE ops indexing a qc_mgate table (matrix pointer
+    into a kept-alive complex128 buffer, interleaved re/im, row-major)."""
+    import numpy as np
+    import qcgen
+    rng = np.random.default_rng(0)
+    U = qcgen.random_unitary(8, rng)
+    ops = [qcgen.Op("H", (0,)), qcgen.Op("MCU", (4, 1, 2, 0, 3), matrix=U, nctrl=2, ctrl_state=2),
+           qcgen.Op("MCU", (5,), matrix=np.eye(2), nctrl=0)]
+    a = qc.encode_ops(ops)
+    assert a[1]["op"] == qc.QC_MGATE and a[1]["qubits"][0] == 0 and a[2]["qubits"][0] == 1
+    mt = a.mtab
+    assert len(mt) == 2 and mt[0]["n_ctrl"] == 2 and mt[0]["n_targ"] == 3
+    assert list(mt[0]["qubits"][:5]) == [4, 1, 2, 0, 3] and mt[0]["ctrl_state"] == 2
+    back = np.ctypeslib.as_array(ctypes.cast(int(mt[0]["matrix"]), ctypes.POINTER(ctypes.c_double)),
+                                 shape=(128,))
+    assert np.array_equal(back[0::2] + 1j * back[1::2], U.reshape(-1))
 
 
 def test_encode_ops_roundtrip():

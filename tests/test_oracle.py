@@ -369,3 +369,100 @@ def test_empty_circuit_and_double_x():
     phi = rstate(4)
     assert np.array_equal(oracle.run(4, phi, []), phi)
     assert np.array_equal(oracle.run(4, phi, [Op("X", (2,)), Op("X", (2,))]), phi)
+
+
+# ------------------------------------------------- generic gates
+def _embedded_mcu(nctrl, k, U, ctrl_state):
+    """Independent construction of the generic gate's 2^nq x 2^nq operator over
+    its listed qubits (controls first, MSB first): identity except the block
+    whose control bits equal ctrl_state, which holds U."""
+    nq = nctrl + k
+    E = np.eye(1 << nq, dtype=complex)
+    cpat = 0
+    for t in range(nctrl):  # listed control t = bit nq-1-t of the local index
+        cpat |= ((ctrl_state >> t) & 1) << (nq - 1 - t)
+    rows = [cpat | r for r in range(1 << k)]
+    E[np.ix_(rows, rows)] = U
+    return E
+
+
+@pytest.mark.parametrize("n", [5, 7])
+def test_mcu_equals_tensor_contraction(n):
+    """Generic gate (every further qubit is one more inserted bit)
+    == the embedded operator contracted on the listed axes, any qubit order,
+    0..3 controls, 1..4 targets, every ctrl_state pattern drawn at random."""
+    rng = np.random.default_rng(100 + n)
+    for _ in range(40):
+        k = int(rng.integers(1, 5))
+        c = int(rng.integers(0, min(3, n - k) + 1))
+        qs = tuple(int(q) for q in rng.choice(n, size=k + c, replace=False))
+        U = qcgen.random_unitary(1 << k, rng)
+        cs = int(rng.integers(1 << c))
+        psi = rstate(n, int(rng.integers(1 << 30)))
+        out = oracle.run(n, psi, [Op("MCU", qs, matrix=U, nctrl=c, ctrl_state=cs)])
+        ref = apply_by_tensor(n, _embedded_mcu(c, k, U, cs), qs, psi)
+        assert np.abs(out - ref).max() < 1e-14, (qs, c, cs)
+
+
+def test_mcu_contiguous_equals_kron():
+    """Brute force: listed qubits 0..nq-1 in order -> kron(E, I) (eq:kron)."""
+    rng = np.random.default_rng(5)
+    n = 6
+    for c, k in ((0, 3), (1, 3), (2, 2), (0, 4), (2, 4)):
+        U = qcgen.random_unitary(1 << k, rng)
+        cs = int(rng.integers(1 << c)) if c else 0
+        full = np.kron(_embedded_mcu(c, k, U, cs), np.eye(1 << (n - c - k)))
+        psi = rstate(n, 9 + c + k)
+        out = oracle.run(n, psi, [Op("MCU", tuple(range(c + k)), matrix=U, nctrl=c, ctrl_state=cs)])
+        assert np.abs(out - full @ psi).max() < 1e-14
+
+
+def test_fig_dctrl_1q_generic_u():
+    """fig:dctrl-1q with a generic U: only phi[6], phi[7] change,
+    by exactly U (the doubly controlled gate "touches a quarter")."""
+    c = _tables()["fig_dctrl_1q"]["cases"][0]
+    V = qcgen.random_unitary(2, np.random.default_rng(21))
+    a, b = c["a"][0], c["b"][0]
+    for x in range(8):
+        out = oracle.run(3, basis(3, x), [Op("MCU", tuple(c["qc"]) + (c["qt"],), matrix=V, nctrl=2)])
+        if x == a or x == b:
+            col = 0 if x == a else 1
+            exp = np.zeros(8, complex)
+            exp[a], exp[b] = V[0, col], V[1, col]
+            assert np.abs(out - exp).max() < 1e-15
+        else:
+            assert np.array_equal(out, basis(3, x))
+
+
+def test_mcu_special_cases_and_inverse():
+    """MCU reduces to the named gates (U1, CU1 with either control state, CCX
+    with X, U2) and MCU followed by its adjoint is the identity (unitarity)."""
+    rng = np.random.default_rng(8)
+    n = 5
+    psi = rstate(n, 3)
+    V = qcgen.random_unitary(2, rng)
+    W = qcgen.random_unitary(4, rng)
+    pairs = [
+        (Op("U1", (2,), matrix=V), Op("MCU", (2,), matrix=V, nctrl=0)),
+        (Op("CU1", (4, 1), matrix=V, ctrl_state=0), Op("MCU", (4, 1), matrix=V, nctrl=1, ctrl_state=0)),
+        (Op("CU1", (0, 3), matrix=V), Op("MCU", (0, 3), matrix=V, nctrl=1)),
+        (Op("U2", (3, 1), matrix=W), Op("MCU", (3, 1), matrix=W, nctrl=0)),
+    ] + [(Op("CCX", (1, 4, 2), ctrl_state=cs), Op("MCU", (1, 4, 2), matrix=PX, nctrl=2, ctrl_state=cs))
+         for cs in range(4)]
+    for named, gen in pairs:
+        assert np.array_equal(oracle.run(n, psi, [named]), oracle.run(n, psi, [gen]))
+    ops = qcgen.random_mcu_circuit(n, 30, seed=4, p_mcu=1.0)
+    back = oracle.run(n, oracle.run(n, psi, ops), qcgen.inverse(ops))
+    assert np.abs(back - psi).max() < 1e-13
+
+
+def test_mcu_validation():
+    psi = rstate(4, 1)
+    with pytest.raises(ValueError):
+        Op("MCU", (0, 1), matrix=np.eye(2), nctrl=0)      # 1 target needs 2x2? -> 2 targets need 4x4
+    with pytest.raises(ValueError):
+        Op("MCU", (0, 1, 2, 3, 4), matrix=np.eye(32), nctrl=0)  # > 4 targets
+    bad = Op("MCU", (0, 1), matrix=np.eye(2), nctrl=1)
+    bad.qubits = (0, 0)
+    with pytest.raises(ValueError):
+        oracle.run(4, psi, [bad])
