@@ -323,21 +323,29 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = t_total / args.steps
     value = gamp(ops, n, ms_per_step / 1e3)
 
-    # NVLink: one exchange of the top rank bit with the top local bit, timed alone
+    # NVLink: one exchange of the top rank bit with the top local bit, timed
+    # alone, for both backends (QC_OPT_EXCHANGE 0: NCCL send/recv + ping-pong
+    # staging copies; 1: P2P swap kernel over CUDA IPC mappings)
     ex = None
     if world > 1:
-        torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(4):
-                s.exchange(n - 1, n_loc - 1)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        te = _max_over_ranks(e0.elapsed_time(e1) / 4, world, dev)
+        ex = {}
         bytes_dir = shard_bytes // 2
-        ex = {"ms": te, "bytes_per_direction": bytes_dir, "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9,
-              "frac_of_900": bytes_dir / (te / 1e3) / 1e9 / 900.0, "backend": "nccl send/recv"}
+        for xmode, name in ((0, "nccl_sendrecv_pingpong"), (1, "p2p_swap_kernel")):
+            s.set_option("exchange", xmode)
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                s.exchange(n - 1, n_loc - 1)  # warm-up (P2P: IPC mapping)
+                e0.record(stream)
+                for _ in range(4):
+                    s.exchange(n - 1, n_loc - 1)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            te = _max_over_ranks(e0.elapsed_time(e1) / 4, world, dev)
+            ex[name] = {"ms": te, "bytes_per_direction": bytes_dir,
+                        "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9,
+                        "frac_of_900": bytes_dir / (te / 1e3) / 1e9 / 900.0}
+        s.set_option("exchange", 0)
 
     # ---- e2e: pinned host state in, circuit, full state out, every step
     # (states above 8 GiB share one pinned buffer for input and output: the
