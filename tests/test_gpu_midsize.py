@@ -42,6 +42,8 @@ CASES = {
     "tfxy24_s10": (24, lambda: qcgen.tfxy(24, 10)),
     "qft26": (26, lambda: qcgen.qft(26)),
     "random25_300": (25, lambda: qcgen.random_circuit(25, 300, seed=2024)),
+    # generic gates: up to 4 controls, 1-4 dense targets
+    "mcu24_150": (24, lambda: qcgen.random_mcu_circuit(24, 150, seed=77, max_ctrl=4)),
 }
 
 
