@@ -349,13 +349,25 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e: pinned host state in, circuit, full state out, every step
     # (states above 8 GiB share one pinned buffer for input and output: the
-    # read-back of step i is the upload of step i+1 -- same bytes moved)
-    h_in = torch.empty(shard_bytes, dtype=torch.uint8, pin_memory=True)
-    h_out = h_in if shard_bytes > (8 << 30) else torch.empty(shard_bytes, dtype=torch.uint8, pin_memory=True)
+    # read-back of step i is the upload of step i+1 -- same bytes moved; a
+    # shard larger than this rank's share of host RAM moves in chunks through
+    # a smaller pinned buffer, every byte of the shard still crossing the link
+    # both ways each step)
+    try:
+        import psutil
+        host_cap = int(psutil.virtual_memory().available * 0.6) // int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    except Exception:
+        host_cap = shard_bytes
+    hb = min(shard_bytes, max(host_cap, 1 << 30))
+    hb -= hb % ab
+    h_in = torch.empty(hb, dtype=torch.uint8, pin_memory=True)
+    h_out = h_in if hb < shard_bytes or hb > (8 << 30) else torch.empty(hb, dtype=torch.uint8, pin_memory=True)
     first = rank << n_loc
+    chunk = hb // ab
+    spans = [(first + o, min(chunk, (1 << n_loc) - o)) for o in range(0, 1 << n_loc, chunk)]
     if world > 1:
         s.canonicalize()
-    s.read_ptr(h_in.data_ptr(), 1 << n_loc, first)  # a valid state to start from
+    s.read_ptr(h_in.data_ptr(), spans[0][1], spans[0][0])  # a valid state (first chunk) to start from
     e2e_steps = max(1, min(args.steps, 5 if small else 2))
     torch.cuda.synchronize()
     e_ev = []
@@ -363,11 +375,13 @@ def run_ours(args, rank, world, local_rank):
         for i in range(e2e_steps + 1):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            s.write_ptr(h_in.data_ptr(), 1 << n_loc, first)
+            for f0, cnt in spans:
+                s.write_ptr(h_in.data_ptr(), cnt, f0)
             s.run(arr)
             if world > 1:
                 s.canonicalize()
-            s.read_ptr(h_out.data_ptr(), 1 << n_loc, first)
+            for f0, cnt in spans:
+                s.read_ptr(h_out.data_ptr(), cnt, f0)
             b.record(stream)
             if i > 0:
                 e_ev.append((a, b))
@@ -423,7 +437,7 @@ def run_ours(args, rank, world, local_rank):
                              "the step is a fused pass, timed by CUDA events on the state's stream)"
                              + ("; the step also holds the exchanges" if world > 1 else "")},
         "e2e": {"value": gamp(ops, n, e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": shard_bytes,
-                "d2h_bytes_per_step": shard_bytes, "ms_per_step": e_ms,
+                "d2h_bytes_per_step": shard_bytes, "ms_per_step": e_ms, "pinned_host_buffer_bytes": hb,
                 "path": "qc_state_write (pinned host) + qc_run_circuit + qc_state_read (pinned host), per rank"},
         "clocks": clocks,
     }
@@ -498,6 +512,31 @@ def sweep(args, local_rank):
         res["north_star_n33_c128"]["qft33"] = {
             "ms": round(t, 2), "gates": len(ops), "passes": inf["last_passes"], "jit": inf["last_jit"],
             "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
+        s.close()
+        torch.cuda.empty_cache()
+    # generic dense k-target gates: fused passes of random
+    # dense 2^k x 2^k blocks (FP64 work 8 * 2^k flop/amp per gate) -- the
+    # "is a dense block a real contraction" evaluation -- and the per-gate
+    # DENSEK kernel's HBM rate
+    res["dense_k_blocks_n28_c128"] = {}
+    n = 28
+    rng = np.random.default_rng(5)
+    for k in (2, 3, 4):
+        ops = []
+        for _ in range(40):
+            qs = tuple(int(q) for q in rng.choice(n, size=k, replace=False))
+            ops.append(qcgen.Op("MCU", qs, matrix=qcgen.random_unitary(1 << k, rng), nctrl=0))
+        s = qc.State(n, "c128", device=local_rank)
+        s.init_random(1)
+        t = _time_runs(s, qc.encode_ops(ops), warm=4, reps=3)
+        inf = s.info()
+        alg = inf["last_flops_per_amp"] * float(1 << n) / (t / 1e3) / 1e12
+        s.set_option("fusion", 0)
+        tg = _time_runs(s, qc.encode_ops(ops[:1]), warm=1, reps=5)
+        res["dense_k_blocks_n28_c128"][f"k{k}"] = {
+            "gates": len(ops), "ms": round(t, 3), "passes": inf["last_passes"],
+            "fused_alg_TFLOPs": round(alg, 2), "fused_alg_flops_frac_of_fp64_peak": round(alg / fma["c128"], 4),
+            "per_gate_ms": round(tg, 4), "per_gate_GBps": round(2 * (16 << n) / (tg / 1e3) / 1e9, 1)}
         s.close()
         torch.cuda.empty_cache()
     for prec in ("c128", "c64"):
