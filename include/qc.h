@@ -108,7 +108,8 @@ typedef enum {
                                  0: never (AOT interpreting kernel); 2: from the first run  */
     QC_OPT_ROW_BITS = 7,      /* 0 (default): auto; else contiguous row bits of a fused tile */
     QC_OPT_TMA_MODE = 8,      /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
-                                 request); 1: one cp.async.bulk per row                      */
+                                 request); 1: one cp.async.bulk per row; 2: one 5-D TMA box
+                                 per tile where the tile's bit runs allow it (else gather4)  */
     QC_OPT_REMAP = 9,         /* 1 (default): a fused pass may end by swapping row bits with
                                  tile bits the next pass needs (a relabel, like SWAP);
                                  0: the row bits keep their qubits                           */

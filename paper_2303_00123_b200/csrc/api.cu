@@ -320,11 +320,26 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
   e->perm = fp.perm;
   e->flops_per_amp = plan_flops_per_amp(fp);
-  const bool g4 = s->tma_mode == 0 && make_row_tmap(tmap_base ? tmap_base : s->d, tmap_bits ? tmap_bits : n_plan, rb,
-                                                     s->dbl, &e->tmap);
+  void* tb = tmap_base ? tmap_base : s->d;
+  const int tbits = tmap_bits ? tmap_bits : n_plan;
+  const bool g4 = (s->tma_mode == 0 || s->tma_mode == 2) && make_row_tmap(tb, tbits, rb, s->dbl, &e->tmap);
   for (auto& p : fp.passes) {
     p.desc.g4 = g4 ? 1 : 0;
     p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
+  }
+  if (s->tma_mode == 2) {
+    // one TMA box per tile where the tile's bit runs fit a 5-D tensor map
+    // (else that pass keeps the gather4 rows, or per-row copies)
+    e->tmaps.assign(fp.passes.size(), e->tmap);
+    for (size_t i = 0; i < fp.passes.size(); ++i) {
+      PassDesc& d = fp.passes[i].desc;
+      uint64_t T = (1ull << d.rb) - 1;
+      for (int j = 0; j < d.n_hi; ++j) T |= 1ull << d.hi_pos[j];
+      if (make_box_tmap(tb, tbits, s->dbl, T, &e->tmaps[i], &d)) {
+        d.g4 = 2;
+        d.pshift = 31;
+      }
+    }
   }
   std::vector<uint8_t> blob = pack_plan(fp, s->dbl);
   for (auto& p : fp.passes) e->passes.push_back(p.desc);
@@ -397,8 +412,9 @@ int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64
     PassDesc pd = e->passes[i];
     pd.rank_bits = rank_bits;
     pd.addr_bits = addr_bits;
-    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, e->tmap, e->ctas, st)
-                                      : launch_fused_pass(base, s->dbl, pd, e->d_blob, e->tmap, e->ctas, st);
+    const QcTmap& tm = e->tmaps.empty() ? e->tmap : e->tmaps[i];
+    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, tm, e->ctas, st)
+                                      : launch_fused_pass(base, s->dbl, pd, e->d_blob, tm, e->ctas, st);
     if (r) return r;
   }
   return 0;
@@ -910,7 +926,7 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       s->row_bits = (int)v;
       break;
     case QC_OPT_TMA_MODE:
-      if (v < 0 || v > 1) return fail(QC_ERR_INVALID_ARG, "tma mode must be 0 or 1");
+      if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "tma mode must be 0, 1 or 2");
       s->tma_mode = (int)v;
       break;
     case QC_OPT_REMAP: s->remap = v != 0; break;

@@ -93,6 +93,35 @@ __device__ __forceinline__ void qc_scatter4(const QcTmap* tm, int32_t r0, int32_
       "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(qc_saddr(src))
       : "memory");
 }
+// One 5-D TMA box (the whole tile) per request: dims in ascending physical
+// bit order, so the box lands in smem in tile-local index order.
+__device__ __forceinline__ void qc_box_load(void* dst, const QcTmap* tm, const int32_t (&c)[5], uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(qc_saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void qc_box_store(const QcTmap* tm, const int32_t (&c)[5], const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(src))
+               : "memory");
+}
+// Box coordinates of a tile: per dim, the outer bits above its tile run
+// (dim 0 in f64 elements: 2 per complex128 amplitude, 1 per complex64).
+template <typename C>
+__device__ __forceinline__ void qc_box_coords(const PassDesc& pd, uint64_t base, int32_t (&c)[5]) {
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    c[d] = 0;
+    if (d < pd.bx_dims) {
+      const int lo = pd.bx_start[d], w = pd.bx_start[d + 1] - lo;
+      const uint64_t v = (base >> lo) & ((1ull << w) - 1ull);
+      c[d] = (int32_t)(d == 0 ? v * (sizeof(C) / 8) : v);
+    }
+  }
+}
 __device__ __forceinline__ void qc_bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -425,7 +454,13 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
         const uint64_t ip = i - NBUF;
         qc_mbar_wait(&empty[b], (uint32_t)((ip / NBUF) & 1ull));
         const uint64_t base = qc_tile_base(pd, blockIdx.x + ip * gridDim.x) | pd.addr_bits;
-        if (pd.g4) {
+        if (pd.g4 == 2) {
+          if (lane == 0) {
+            int32_t c[5];
+            qc_box_coords<C>(pd, base, c);
+            qc_box_store(tmap, c, buf);
+          }
+        } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)
             qc_scatter4(tmap, (int32_t)((base | row_off[r]) >> rb), (int32_t)((base | row_off[r + 1]) >> rb),
                         (int32_t)((base | row_off[r + 2]) >> rb), (int32_t)((base | row_off[r + 3]) >> rb),
@@ -447,7 +482,13 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
           qc_mbar_arrive_expect_tx(&full[b], tile_bytes);
         }
         __syncwarp();
-        if (pd.g4) {
+        if (pd.g4 == 2) {
+          if (lane == 0) {
+            int32_t c[5];
+            qc_box_coords<C>(pd, base, c);
+            qc_box_load(buf, tmap, c, &full[b]);
+          }
+        } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)
             qc_gather4(buf + row_at(r), tmap, (int32_t)((base | row_off[r]) >> rb),
                        (int32_t)((base | row_off[r + 1]) >> rb), (int32_t)((base | row_off[r + 2]) >> rb),

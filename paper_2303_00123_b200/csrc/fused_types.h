@@ -78,7 +78,8 @@ struct alignas(64) QcTmap {
 struct PassDesc {
   int32_t k, rb;          // tile bits, row bits (T contains physical 0..rb-1)
   int32_t pshift;         // smem: one 16-byte pad every 2^pshift amplitudes
-  int32_t g4;             // 1: rows move by TMA tile::gather4 / scatter4 (4 rows per request)
+  int32_t g4;             // tile transport: 0 one cp.async.bulk per row; 1 TMA tile::gather4 /
+                          // scatter4 (4 rows per request); 2 one TMA box per tile (bx_*)
   int32_t n_hi;           // k - rb
   int32_t n_outer;
   int32_t hi_pos[16];     // physical bit of tile-local bit rb+j
@@ -89,6 +90,9 @@ struct PassDesc {
   uint32_t n_sub, n_ops, n_prun;
   uint32_t off_hdr, off_coef, off_term;  // section offsets inside the pass blob
   uint32_t pad_;
+  int32_t bx_dims;        // g4 == 2: dims of the pass's 5-D tensor map; dim d spans physical
+  int32_t bx_start[6];    // bits [bx_start[d], bx_start[d+1]): its tile bits (the box) below,
+                          // outer bits (the coordinate) above
   uint64_t rank_bits;     // sharded state: this rank's global bits (rank << n_loc), OR-ed
                           // into every tile's base for predicates / diagonal bits only
   uint64_t addr_bits;     // OR-ed into amplitude addresses (loopback: shards share one buffer)

@@ -297,6 +297,74 @@ int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_b
              : launch_t<float>(state, pd, d_blob, tm, ctas, st);
 }
 
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encoder() {
+  static EncodeFn enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<EncodeFn>(fn);
+  }
+  return enc;
+}
+}  // namespace
+
+// 5-D tensor map that moves one whole tile per TMA request (PassDesc g4 == 2).
+// The tile's bit set T (physical bits of an nbits-bit index) splits into runs
+// of consecutive bits; dim d starts at run d and extends up to the next run,
+// so its box covers the run and its coordinate selects the outer bits above
+// it.  Runs longer than a box dimension allows (256 elements) are split.
+// Returns false if that needs more than 5 dims.
+bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t T, QcTmap* out, PassDesc* d) {
+  EncodeFn enc = encoder();
+  if (!enc || !(T & 1ull)) return false;
+  const int epa = dbl ? 2 : 1;                // f64 elements per amplitude
+  const int max0 = dbl ? 7 : 8, maxd = 8;    // box dim <= 256 elements
+  int start[8], len[8], nd = 0;               // tile runs
+  for (int p = 0; p < nbits; ++p) {
+    if (!((T >> p) & 1ull)) continue;
+    if (nd && start[nd - 1] + len[nd - 1] == p && len[nd - 1] < (nd == 1 ? max0 : maxd)) {
+      ++len[nd - 1];
+    } else {
+      if (nd == 5) return false;
+      start[nd] = p;
+      len[nd] = 1;
+      ++nd;
+    }
+  }
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    if (i < nd) {
+      const int end = i + 1 < nd ? start[i + 1] : nbits;
+      gdim[i] = ((cuuint64_t)1 << (end - start[i])) * (i == 0 ? epa : 1);
+      box[i] = (cuuint32_t)((1u << len[i]) * (i == 0 ? epa : 1));
+      if (i) gstride[i - 1] = ((cuuint64_t)8 * epa) << start[i];
+      d->bx_start[i] = start[i];
+    } else {
+      gdim[i] = 1;
+      box[i] = 1;
+      gstride[i - 1] = 16;
+    }
+  }
+  d->bx_dims = nd;
+  d->bx_start[nd] = nbits;
+  CUtensorMap tm;
+  const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  memcpy(out, &tm, sizeof tm);
+  return true;
+}
+
 // 2D tensor map over the state: rows of 2^rb amplitudes (as f64 elements) x
 // 2^(n-rb) rows, box = one row; used with tile::gather4 / scatter4.
 bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out) {

@@ -154,6 +154,7 @@ int launch_gate(void* state, int n, bool dbl, const PGate& g, void* stream);
 int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_blob, const QcTmap& tm,
                       int ctas, void* stream);
 bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out);
+bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t tile_bits_set, QcTmap* out, PassDesc* d);
 int fused_configure(bool dbl);
 int launch_init_random(void* state, int n, bool dbl, uint64_t seed, void* stream, uint64_t first = 0,
                        uint64_t count = 0);

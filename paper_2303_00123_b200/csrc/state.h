@@ -23,6 +23,7 @@ struct PlanEntry {
   std::vector<JitKernel> jit;
   int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
   QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
+  std::vector<QcTmap> tmaps;         // per-pass box tensor maps (PassDesc g4 == 2; empty otherwise)
   bool dbl = true;
   int64_t relabels = 0;
   int uses = 0;
