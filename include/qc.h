@@ -106,10 +106,14 @@ typedef enum {
     QC_OPT_BLOCK_FUSION = 5,  /* 1 (default): merge gates on <= 2 qubits into exact blocks    */
     QC_OPT_JIT = 6,           /* 1 (default): specialise repeated fused plans with NVRTC;
                                  0: never (AOT interpreting kernel); 2: from the first run  */
-    QC_OPT_ROW_BITS = 7,      /* 0 (default): auto; else contiguous row bits of a fused tile */
-    QC_OPT_TMA_MODE = 8,      /* 0 (default): rows by TMA tile::gather4/scatter4 (4 rows per
-                                 request); 1: one cp.async.bulk per row; 2: one 5-D TMA box
-                                 per tile where the tile's bit runs allow it (else gather4)  */
+    QC_OPT_ROW_BITS = 7,      /* 0 (default): auto -- with the box transport the planner plans
+                                 3..6 (c128) / 4..7 (c64) row bits and keeps the plan a host
+                                 cost model prefers; else the contiguous row bits of a tile  */
+    QC_OPT_TMA_MODE = 8,      /* 0 (default): one 5-D TMA box per tile (dims = the runs of
+                                 consecutive tile bits, coordinates = the outer bits above
+                                 each run; several boxes when > 5 runs), gather4 rows for a
+                                 pass whose runs do not fit; 1: one cp.async.bulk per row;
+                                 2: TMA tile::gather4/scatter4 rows only (4 rows/request)    */
     QC_OPT_REMAP = 9,         /* 1 (default): a fused pass may end by swapping row bits with
                                  tile bits the next pass needs (a relabel, like SWAP);
                                  0: the row bits keep their qubits                           */

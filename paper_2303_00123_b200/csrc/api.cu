@@ -297,6 +297,76 @@ void plan_geometry(const qc_state* s, int n_plan, int* k_out, int* rb_out, int* 
   *ctas_out = s->ctas ? s->ctas : sm_count();
 }
 
+// Tile bit set of a planned pass: the row bits plus its hi bits.
+uint64_t pass_tile_set(const PassDesc& d) {
+  uint64_t T = (1ull << d.rb) - 1;
+  for (int j = 0; j < d.n_hi; ++j) T |= 1ull << d.hi_pos[j];
+  return T;
+}
+
+// Host cost model of a plan (seconds per amplitude-normalised unit): per pass
+// sqrt(H^2 + F^2), H = 2 Ns / the transport's rate, F = its fused flops / the
+// ALU rate.  Rates from round-2 B200 measurements: TMA box
+// transport 4.1 / 4.55 / 5.3 / 5.7 TB/s when the tile's innermost run is 64 /
+// 128 / 256 / >= 512 B; gather4 rows 5.6 (1 KiB), 4.6 (512 B), 3.5 (less);
+// fused passes ~26 (c128) / ~45 (c64) algorithmic TFLOP/s.
+double plan_cost_model(const FusedPlan& fp, int n, bool dbl, bool box) {
+  const double ab = dbl ? 16 : 8, N = std::ldexp(1.0, n);
+  double t = 0;
+  for (const FusedPassPlan& pp : fp.passes) {
+    const PassDesc& d = pp.desc;
+    const uint64_t T = pass_tile_set(d);
+    PassDesc tmp = d;
+    double bw;
+    if (box && make_box_tmap(nullptr, n, dbl, T, nullptr, &tmp)) {
+      const int run0 = std::countr_one(T);
+      const double inner = ab * std::ldexp(1.0, std::min(run0, dbl ? 7 : 8));
+      bw = inner <= 64 ? 4.1e12 : inner <= 128 ? 4.55e12 : (inner <= 256 ? 5.3e12 : 5.7e12);
+    } else {
+      const double row = ab * std::ldexp(1.0, d.rb);
+      bw = row >= 1024 ? 5.6e12 : (row >= 512 ? 4.6e12 : 3.5e12);
+    }
+    const double H = 2 * ab * N / bw, F = pass_flops_per_amp(pp) * N / (dbl ? 26e12 : 45e12);
+    t += std::sqrt(H * H + F * F);
+  }
+  return t;
+}
+
+// Plan the blocks; with row_bits 0 in the box transport, try several row
+// widths (narrow rows leave more free tile bits per pass -> fewer passes,
+// but slower rows) and keep the plan the cost model prefers -- the widest
+// rows within 2 % of the cheapest (the model is only that accurate).
+FusedPlan plan_best(int n_plan, int k, int rb_default, int row_bits_opt, bool box, bool dbl,
+                    const std::vector<PGate>& blocks, bool remap, int* rb_out) {
+  std::vector<int> cands;
+  if (row_bits_opt || !box || n_plan <= k) cands.push_back(rb_default);
+  else cands = dbl ? std::vector<int>{3, 4, 5, 6} : std::vector<int>{3, 4, 5, 6, 7};
+  int need_max = 0;  // a tile holds the row bits plus every non-diagonal target of a gate
+  for (const PGate& g : blocks) need_max = std::max(need_max, g.kind == GK::DIAG1 ? 0 : std::popcount(pgate_targets(g)));
+  FusedPlan best;
+  double best_cost = 1e300;
+  int best_rb = -1;
+  for (int rb : cands) {
+    if (rb > k - 2) rb = k - 2;
+    if (rb + need_max > k) rb = k - need_max;
+    if (rb < 1) rb = 1;
+    if (rb == best_rb) continue;
+    FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap, pass_flops_budget(dbl));
+    if (!fp.ok) continue;
+    const double c = plan_cost_model(fp, n_plan, dbl, box);
+    if (getenv("QC_PLAN_DEBUG"))
+      fprintf(stderr, "plan_best: rb %d -> %zu passes, model %.1f ms\n", rb, fp.passes.size(), c * 1e3);
+    if (c < best_cost * (best_rb < 0 ? 1.0 : 1.02)) {  // candidates ascend: wider wins near-ties
+      best_cost = std::min(c, best_cost);
+      best_rb = rb;
+      best = std::move(fp);
+    }
+  }
+  if (best_rb < 0) best.ok = false;
+  *rb_out = best_rb;
+  return best;
+}
+
 // Fuse + plan + pack + upload lowered gates over n_plan local bits (bits at or
 // above n_plan -- the rank bits of a sharded state -- may appear only as
 // controls / diagonal bits).  `tmap_base` / `tmap_bits`: the buffer and index
@@ -310,13 +380,8 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
   e->fused_gates = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  // a tile holds the row bits plus every non-diagonal target of a gate: a
-  // generic gate's 3-4 targets may need narrower rows in a small tile
-  for (const PGate& g : blocks) {
-    const int need = g.kind == GK::DIAG1 ? 0 : std::popcount(pgate_targets(g));
-    if (rb + need > k) rb = std::max(1, k - need);
-  }
-  FusedPlan fp = plan_fused(n_plan, k, rb, blocks, remap, pass_flops_budget(s->dbl));
+  const bool box = s->tma_mode == 0;
+  FusedPlan fp = plan_best(n_plan, k, rb, s->row_bits, box, s->dbl, blocks, remap, &rb);
   if (!fp.ok) return fail(QC_ERR_UNSUPPORTED, "planner failed (k=%d rb=%d)", k, rb);
   e->perm = fp.perm;
   e->flops_per_amp = plan_flops_per_amp(fp);
@@ -327,15 +392,13 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
     p.desc.g4 = g4 ? 1 : 0;
     p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
   }
-  if (s->tma_mode == 2) {
+  if (box) {
     // one TMA box per tile where the tile's bit runs fit a 5-D tensor map
     // (else that pass keeps the gather4 rows, or per-row copies)
     e->tmaps.assign(fp.passes.size(), e->tmap);
     for (size_t i = 0; i < fp.passes.size(); ++i) {
       PassDesc& d = fp.passes[i].desc;
-      uint64_t T = (1ull << d.rb) - 1;
-      for (int j = 0; j < d.n_hi; ++j) T |= 1ull << d.hi_pos[j];
-      if (make_box_tmap(tb, tbits, s->dbl, T, &e->tmaps[i], &d)) {
+      if (make_box_tmap(tb, tbits, s->dbl, pass_tile_set(d), &e->tmaps[i], &d)) {
         d.g4 = 2;
         d.pshift = 31;
       }
@@ -1008,16 +1071,20 @@ extern "C" qc_status qc_debug_plan(int n, qc_precision p, const qc_gate* ops, si
   std::vector<PGate> blocks = block_fusion ? fuse_blocks(gates, ~0ull) : gates;
   out->blocks = (int64_t)blocks.size();
   if (blocks.empty()) return QC_OK;
-  FusedPlan fp = plan_fused(n, k, rb, blocks, remap != 0, pass_flops_budget(dbl));
+  FusedPlan fp = plan_best(n, k, rb, row_bits, true, dbl, blocks, remap != 0, &rb);  // default transport
   if (!fp.ok) return err(QC_ERR_UNSUPPORTED, "planner failed");
   out->remap_swaps = fp.remap_swaps;
   out->flops_per_amp = plan_flops_per_amp(fp);
   out->restore_passes = fp.restore_passes;
-  // mirror build_fused_entry's layout choice (make_row_tmap's gather4 limits)
+  // mirror build_fused_entry's layout choice (boxes, else make_row_tmap's gather4 limits)
   const bool g4 = ((uint64_t)(dbl ? 16 : 8) << rb) <= 1024 && n - rb <= 31 && n - rb >= 2;
   for (auto& pp : fp.passes) {
     pp.desc.g4 = g4 ? 1 : 0;
     pp.desc.pshift = g4 ? 31 : rb;
+    if (make_box_tmap(nullptr, n, dbl, pass_tile_set(pp.desc), nullptr, &pp.desc)) {
+      pp.desc.g4 = 2;
+      pp.desc.pshift = 31;
+    }
   }
   out->passes = (int64_t)fp.passes.size();
   const int LB = dbl ? 3 : 4;  // tile bits inside one 16-B / 8-B bank-group phase (jit.cu)

@@ -458,7 +458,14 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
           if (lane == 0) {
             int32_t c[5];
             qc_box_coords<C>(pd, base, c);
-            qc_box_store(tmap, c, buf);
+            const int32_t c4 = c[4];
+            uint32_t v = 0, j = 0;
+            do {  // every combination of the extra tile bits (one box if none)
+              c[4] = c4 | (int32_t)v;
+              qc_box_store(tmap, c, buf + ((size_t)j << pd.bx_sub));
+              v = (v - pd.bx_xmask) & pd.bx_xmask;
+              ++j;
+            } while (v);
           }
         } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)
@@ -486,7 +493,14 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
           if (lane == 0) {
             int32_t c[5];
             qc_box_coords<C>(pd, base, c);
-            qc_box_load(buf, tmap, c, &full[b]);
+            const int32_t c4 = c[4];
+            uint32_t v = 0, j = 0;
+            do {
+              c[4] = c4 | (int32_t)v;
+              qc_box_load(buf + ((size_t)j << pd.bx_sub), tmap, c, &full[b]);
+              v = (v - pd.bx_xmask) & pd.bx_xmask;
+              ++j;
+            } while (v);
           }
         } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128)

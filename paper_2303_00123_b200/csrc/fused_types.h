@@ -93,6 +93,8 @@ struct PassDesc {
   int32_t bx_dims;        // g4 == 2: dims of the pass's 5-D tensor map; dim d spans physical
   int32_t bx_start[6];    // bits [bx_start[d], bx_start[d+1]): its tile bits (the box) below,
                           // outer bits (the coordinate) above
+  uint32_t bx_xmask;      // tile bits beyond the 5th run, relative to bx_start[4]: one box per
+  int32_t bx_sub;         // combination of them; each box holds 2^bx_sub amplitudes
   uint64_t rank_bits;     // sharded state: this rank's global bits (rank << n_loc), OR-ed
                           // into every tile's base for predicates / diagonal bits only
   uint64_t addr_bits;     // OR-ed into amplitude addresses (loopback: shards share one buffer)

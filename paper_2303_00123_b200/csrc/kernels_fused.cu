@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <bit>
 #include <cstring>
 
 #include "fused_common.cuh"
@@ -321,24 +322,37 @@ EncodeFn encoder() {
 // of consecutive bits; dim d starts at run d and extends up to the next run,
 // so its box covers the run and its coordinate selects the outer bits above
 // it.  Runs longer than a box dimension allows (256 elements) are split.
-// Returns false if that needs more than 5 dims.
+// Tile bits beyond the 5th run stay in dim 4's coordinate: one box per
+// combination of them (they are the tile's top bits, so each box is a
+// contiguous slice of the tile in smem).
+// base == nullptr: layout only (host planning; no driver call).
 bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t T, QcTmap* out, PassDesc* d) {
-  EncodeFn enc = encoder();
-  if (!enc || !(T & 1ull)) return false;
+  EncodeFn enc = base ? encoder() : nullptr;
+  if ((base && !enc) || !(T & 1ull)) return false;
   const int epa = dbl ? 2 : 1;                // f64 elements per amplitude
   const int max0 = dbl ? 7 : 8, maxd = 8;    // box dim <= 256 elements
-  int start[8], len[8], nd = 0;               // tile runs
+  int start[64], len[64], nr = 0;             // tile runs
   for (int p = 0; p < nbits; ++p) {
     if (!((T >> p) & 1ull)) continue;
-    if (nd && start[nd - 1] + len[nd - 1] == p && len[nd - 1] < (nd == 1 ? max0 : maxd)) {
-      ++len[nd - 1];
+    if (nr && start[nr - 1] + len[nr - 1] == p && len[nr - 1] < (nr == 1 ? max0 : maxd)) {
+      ++len[nr - 1];
     } else {
-      if (nd == 5) return false;
-      start[nd] = p;
-      len[nd] = 1;
-      ++nd;
+      start[nr] = p;
+      len[nr] = 1;
+      ++nr;
     }
   }
+  const int nd = nr < 5 ? nr : 5;
+  uint32_t xmask = 0;
+  int sub = 0;
+  for (int i = 0; i < nr; ++i) {
+    if (i < nd) {
+      sub += len[i];
+      continue;
+    }
+    for (int b = 0; b < len[i]; ++b) xmask |= 1u << (start[i] + b - start[4]);
+  }
+  if (std::popcount(xmask) > 4) return false;  // > 16 boxes per tile: keep the gather4 rows
   cuuint64_t gdim[5], gstride[4];
   cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
   for (int i = 0; i < 5; ++i) {
@@ -356,6 +370,9 @@ bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t T, QcTmap* out, Pas
   }
   d->bx_dims = nd;
   d->bx_start[nd] = nbits;
+  d->bx_xmask = xmask;
+  d->bx_sub = sub;
+  if (!base) return true;
   CUtensorMap tm;
   const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstride, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -835,9 +835,14 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
   for (int p = 0; p < n; ++p)
     if (plan.perm[p] != p) plan.ok = false;  // (cannot happen: every pass fixes >= 1 move)
   if (getenv("QC_PLAN_DEBUG"))
-    for (size_t i = 0; i < plan.passes.size(); ++i)
-      fprintf(stderr, "pass %zu: subs %zu ops %zu flops/amp %.1f\n", i, plan.passes[i].subs.size(),
-              plan.passes[i].ops.size(), pass_flops_per_amp(plan.passes[i]));
+    for (size_t i = 0; i < plan.passes.size(); ++i) {
+      const PassDesc& d = plan.passes[i].desc;
+      uint64_t T = (1ull << d.rb) - 1;
+      for (int j = 0; j < d.n_hi; ++j) T |= 1ull << d.hi_pos[j];
+      const int runs = popc(T & ~(T << 1));  // runs of consecutive tile bits (TMA box dims)
+      fprintf(stderr, "pass %zu: subs %zu ops %zu flops/amp %.1f runs %d\n", i, plan.passes[i].subs.size(),
+              plan.passes[i].ops.size(), pass_flops_per_amp(plan.passes[i]), runs);
+    }
   return plan;
 }
 

@@ -12,12 +12,25 @@ def test_debug_symbol_exported():
 
 
 def test_qft30_plan_shape():
-    st = qc.debug_plan(30, qcgen.qft(30))
+    # 1 KiB rows (rb = 6): 6 free tile bits per pass -> H(0..6), ..., H(21..29)
+    st = qc.debug_plan(30, qcgen.qft(30), row_bits=6)
     assert st["gates"] == 480 and st["relabels"] == 15
-    # 7 high tile bits per pass: H(0..6), H(7..13), H(14..20), H(21..29)
     assert st["passes"] == 4
     assert st["phase_runs"] > 0
     assert st["blob_bytes"] > 0
+    # auto row bits (box transport): narrower rows, 9 free tile bits -> 3 passes
+    assert qc.debug_plan(30, qcgen.qft(30))["passes"] == 3
+
+
+def test_auto_row_bits_follows_the_cost_model():
+    """Row bits 0 = auto: the planner tries 3..6 row bits and keeps the plan
+    the host cost model prefers -- never more passes than the 1 KiB-row plan,
+    and the 137 GB TFXY-33 headline drops from 23 to 17 passes."""
+    for n, ops in ((30, qcgen.tfxy(30, 10)), (33, qcgen.tfxy(33, 10)), (33, qcgen.qft(33))):
+        auto = qc.debug_plan(n, ops)["passes"]
+        wide = qc.debug_plan(n, ops, row_bits=6)["passes"]
+        assert auto <= wide
+    assert qc.debug_plan(33, qcgen.tfxy(33, 10))["passes"] == 17
 
 
 def test_tfxy_block_fusion_merges_pair_blocks():
@@ -71,8 +84,9 @@ def test_remap_cuts_tfxy_passes(n, prec):
     passes when the row bits may change qubits between passes; the plan ends
     in the layout it started from (restore passes counted in `passes`)."""
     ops = qcgen.tfxy(n, 10)
-    on = qc.debug_plan(n, ops, precision=prec)
-    off = qc.debug_plan(n, ops, precision=prec, remap=False)
+    rb = 6 if prec == "c128" else 7  # same row geometry for both (auto row bits would differ)
+    on = qc.debug_plan(n, ops, precision=prec, row_bits=rb)
+    off = qc.debug_plan(n, ops, precision=prec, remap=False, row_bits=rb)
     assert off["remap_swaps"] == 0 and off["restore_passes"] == 0
     assert on["remap_swaps"] > 0
     assert on["passes"] * 2 <= off["passes"], (on, off)
