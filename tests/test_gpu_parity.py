@@ -355,9 +355,11 @@ def test_remap_matches_oracle_and_restores_layout(qcmod, prec, n, tile_bits, cir
     ops = {"tfxy": lambda: qcgen.tfxy(n, 4), "qft": lambda: qcgen.qft(n),
            "random": lambda: qcgen.random_circuit(n, 300, seed=900 + n)}[circ]()
     ref = ref_run(n, prec, ops)
+    rb = 6 if prec == "c128" else 7  # fixed 1 KiB rows: the remap path is what is under test
     for jit in (0, 2):
         with qcmod.State(n, prec) as s:
             s.set_option("tile_bits", tile_bits)
+            s.set_option("row_bits", rb)
             s.set_option("jit", jit)
             s.set_option("relabel_swap", 0)  # so the only relabelling is the remap
             s.init_random(qcgen.STATE_SEED)
@@ -366,7 +368,7 @@ def test_remap_matches_oracle_and_restores_layout(qcmod, prec, n, tile_bits, cir
             got = s.read()
         assert info["layout_is_canonical"], info
         assert maxerr(got, ref) <= TOL[prec], (jit, maxerr(got, ref))
-    st = qcmod.qc.debug_plan(n, ops, precision=prec, tile_bits=tile_bits)
+    st = qcmod.qc.debug_plan(n, ops, precision=prec, tile_bits=tile_bits, row_bits=rb)
     if circ != "qft":
         assert st["remap_swaps"] > 0, st
 
