@@ -59,6 +59,15 @@ qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* o
  * updated.  Used to time NVLink exchanges in isolation. */
 qc_status qc_debug_exchange(qc_state* s, int g, int l);
 
+/* The TMA box decomposition of a tile (host only; QC_OPT_TMA_MODE 0): the
+ * tile's physical bit set T over an nbits-bit index -> dims (<= 5) starting
+ * at starts[0..dims) (starts[dims] = nbits), box widths boxbits[d] (tile bits
+ * at the bottom of dim d), and xmask = tile bits beyond the 5th run relative
+ * to starts[4] (one box per combination).  Returns QC_ERR_UNSUPPORTED if the
+ * tile needs more than 16 boxes (the pass then moves gather4 rows). */
+qc_status qc_debug_box_layout(uint64_t tile_bits_set, int nbits, int dbl, int* dims, int* starts,
+                              int* boxbits, uint32_t* xmask);
+
 /* Measurement utility (needs a GPU): the FMA throughput of the current device
  * in TFLOP/s (2 flops per FMA), FP64 (dbl != 0) or FP32, from a kernel of 8
  * independent FMA chains per thread (best of 3 timed launches).  bench.py

@@ -1152,6 +1152,22 @@ extern "C" qc_status qc_debug_exchange(qc_state* s, int g, int l) {
   return QC_OK;
 }
 
+extern "C" qc_status qc_debug_box_layout(uint64_t T, int nbits, int dbl, int* dims, int* starts, int* boxbits,
+                                         uint32_t* xmask) {
+  if (!dims || !starts || !boxbits || !xmask) return fail(QC_ERR_INVALID_ARG, "NULL argument");
+  if (nbits < 1 || nbits > 62 || (T >> nbits)) return fail(QC_ERR_INVALID_ARG, "bad tile set");
+  PassDesc d{};
+  if (!make_box_tmap(nullptr, nbits, dbl != 0, T, nullptr, &d)) return fail(QC_ERR_UNSUPPORTED, "no box layout");
+  *dims = d.bx_dims;
+  for (int i = 0; i <= d.bx_dims; ++i) starts[i] = d.bx_start[i];
+  for (int i = 0; i < d.bx_dims; ++i) {
+    const uint64_t in_dim = ((T >> d.bx_start[i]) & ((1ull << (d.bx_start[i + 1] - d.bx_start[i])) - 1));
+    boxbits[i] = std::countr_one(in_dim);
+  }
+  *xmask = d.bx_xmask;
+  return QC_OK;
+}
+
 extern "C" qc_status qc_debug_fma_peak(int dbl, double* tflops) {
   if (!tflops) return fail(QC_ERR_INVALID_ARG, "tflops is NULL");
   const int r = fma_peak(dbl != 0, tflops);

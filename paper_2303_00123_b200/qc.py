@@ -87,7 +87,7 @@ class qc_plan_stats(ctypes.Structure):
 
 
 DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange",
-                 "qc_debug_fma_peak"]
+                 "qc_debug_fma_peak", "qc_debug_box_layout"]
 
 _lib = None
 
@@ -133,6 +133,9 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_dist_schedule.restype = ctypes.c_int
     L.qc_debug_exchange.argtypes = [vp, i32, i32]
     L.qc_debug_exchange.restype = ctypes.c_int
+    L.qc_debug_box_layout.argtypes = [u64, i32, i32, ctypes.POINTER(ctypes.c_int), vp, vp,
+                                      ctypes.POINTER(ctypes.c_uint32)]
+    L.qc_debug_box_layout.restype = ctypes.c_int
     L.qc_debug_fma_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double)]
     L.qc_debug_fma_peak.restype = ctypes.c_int
     L.qc_last_error.restype = ctypes.c_char_p
@@ -390,6 +393,20 @@ def debug_plan(n: int, ops, precision: str = "c128", tile_bits: int = 0, block_f
     if rc != QC_OK:
         raise QCError(rc, eb.value.decode())
     return {f: getattr(st, f) for f, _ in qc_plan_stats._fields_}
+
+
+def debug_box_layout(tile_set: int, nbits: int, dbl: bool = True):
+    """(starts[0..dims], boxbits[0..dims), xmask) of a tile's TMA box layout, or None."""
+    dims = ctypes.c_int(0)
+    starts = np.zeros(8, dtype=np.int32)
+    boxbits = np.zeros(8, dtype=np.int32)
+    xm = ctypes.c_uint32(0)
+    rc = lib().qc_debug_box_layout(tile_set, nbits, int(dbl), ctypes.byref(dims), starts.ctypes.data,
+                                   boxbits.ctypes.data, ctypes.byref(xm))
+    if rc == QC_ERR_UNSUPPORTED:
+        return None
+    _check(rc)
+    return [int(x) for x in starts[:dims.value + 1]], [int(x) for x in boxbits[:dims.value]], int(xm.value)
 
 
 def fma_peak(dbl: bool = True) -> float:

@@ -409,3 +409,21 @@ def test_qasm_program_on_gpu(qcmod):
             s.run(arr)
             got = s.read()
         assert maxerr(got, ref_run(n, prec, ops)) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("tma,rb", [(0, 0), (0, 2), (0, 3), (0, 4), (2, 6), (1, 5)])
+def test_tile_transports_match_oracle(qcmod, prec, tma, rb):
+    """Every tile transport (0: one TMA box per tile -- several when a tile
+    has > 5 bit runs, narrow rows; 2: gather4 rows; 1: one bulk copy per row)
+    and row width gives the oracle's result on QFT, TFXY and random circuits,
+    interpreting (1st run) and NVRTC (2nd) kernels."""
+    for n, ops in ((19, qcgen.qft(19)), (20, qcgen.tfxy(20, 6)), (18, qcgen.random_circuit(18, 250, seed=21))):
+        ref = ref_run(n, prec, ops)
+        with qcmod.State(n, prec) as s:
+            s.set_option("tma_mode", tma)
+            s.set_option("row_bits", rb)
+            for _ in range(2):
+                s.init_random(qcgen.STATE_SEED)
+                s.run(ops)
+                assert maxerr(s.read(), ref) <= TOL[prec], (n, tma, rb)

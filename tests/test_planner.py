@@ -97,3 +97,47 @@ def test_remap_off_below_tile():
     # whole state in one tile: no passes to remap between
     st = qc.debug_plan(10, qcgen.tfxy(10, 10))
     assert st["passes"] == 1 and st["remap_swaps"] == 0
+
+
+def _box_tile_indices(layout, nbits):
+    """Tile-local order of the amplitudes the box(es) cover, rebuilt from the
+    layout alone: dims ascending, box d covers boxbits[d] bits above
+    starts[d]; extra (xmask) bits above dim 4's box, one box per value."""
+    starts, boxbits, xmask = layout
+    offs = [0]
+    for d, w in enumerate(boxbits):
+        offs = [o | (i << starts[d]) for i in range(1 << w) for o in offs]
+    xs = [0]
+    for b in range(32):
+        if (xmask >> b) & 1:
+            xs = xs + [x | (1 << (starts[4] + b)) for x in xs]
+    return sorted(x | o for x in xs for o in offs), len(xs)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_box_layout_covers_the_tile_in_local_order(seed):
+    """TMA box transport: the decomposition of a random tile bit set T into
+    <= 5 tensor-map dims (+ boxes over the bits beyond the 5th run) covers
+    exactly the 2^|T| amplitudes of the tile, each once; a tile's local index
+    order (ascending physical bits) is the boxes' linear order."""
+    rng = np.random.default_rng(seed)
+    nbits = int(rng.integers(14, 34))
+    for dbl in (True, False):
+        for _ in range(20):
+            rb = int(rng.integers(1, 7))
+            hi = rng.choice(np.arange(rb, nbits), size=12 - rb, replace=False)
+            T = (1 << rb) - 1
+            for p in hi:
+                T |= 1 << int(p)
+            lay = qc.debug_box_layout(T, nbits, dbl)
+            runs = bin(T & ~(T << 1)).count("1")
+            if lay is None:
+                assert runs > 5  # only tiles with too many runs fall back
+                continue
+            starts, boxbits, xmask = lay
+            assert len(boxbits) <= 5 and starts[0] == 0 and starts[-1] == nbits
+            assert all(w <= (7 if dbl else 8) for w in boxbits[:1]) and all(w <= 8 for w in boxbits)
+            idx, nbox = _box_tile_indices(lay, nbits)
+            tile = sorted(sum(((x >> j) & 1) << int(p) for j, p in enumerate(b for b in range(nbits) if (T >> b) & 1))
+                          for x in range(1 << 12))
+            assert idx == tile and nbox <= 16
