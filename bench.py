@@ -514,6 +514,30 @@ def sweep(args, local_rank):
             "fused_pass_GBps": round(gbps, 1), "fused_pass_frac_of_measured_hbm": round(gbps / peak, 4)}
         s.close()
         torch.cuda.empty_cache()
+    # qubit-swap exchange on one GPU (loopback backend: both shards of a
+    # world-2 state in one buffer, the swap kernel the P2P backend runs over
+    # NVLink, here HBM-local): bytes per direction / time
+    n = 32
+    s = qc.State.loopback(n, "c128", 2)
+    s.init_random(1)
+    st = torch.cuda.ExternalStream(s.stream)
+    with torch.cuda.stream(st):
+        s.exchange(n - 1, n - 2)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(4):
+            s.exchange(n - 1, n - 2)
+        b.record(st)
+        torch.cuda.synchronize()
+    te = a.elapsed_time(b) / 4
+    bytes_dir = (16 << (n - 1)) // 2  # per rank per direction
+    res["exchange_loopback_n32_w2_c128"] = {
+        "ms": round(te, 3), "bytes_per_direction_per_rank": bytes_dir,
+        "swap_kernel_GBps_hbm": round(2 * 2 * bytes_dir / (te / 1e3) / 1e9, 1),
+        "note": "both ranks' halves swapped in place by one kernel: 2 x (read + write) of the exchanged bytes"}
+    s.close()
+    torch.cuda.empty_cache()
     # generic dense k-target gates: fused passes of random
     # dense 2^k x 2^k blocks (FP64 work 8 * 2^k flop/amp per gate) -- the
     # "is a dense block a real contraction" evaluation -- and the per-gate
