@@ -698,6 +698,16 @@ def main():
             n = out["config"]["qubits"]
             out["cpu_baseline"] = cpu_baseline(args.config, n)
             out["cpu_omp_paper_program"] = cpu_omp_curve()
+            # the paper's CPU-vs-GPU comparison (E1/E2) on this box:
+            # the paper's CPU program vs the fused GPU path, same circuits
+            sw = out.get("sweep", {}).get("circuit_ms_vs_qubits", {})
+            cmp = {}
+            for key, ms in out["cpu_omp_paper_program"]["ms"].items():
+                for nq, cpu_ms in ms.items():
+                    g = sw.get(key, {}).get(nq)
+                    if g:
+                        cmp[f"{key}_n{nq}"] = {"cpu_ms": cpu_ms, "gpu_ms": g["ms"], "speedup": round(cpu_ms / g["ms"], 1)}
+            out["cpu_vs_gpu_paper_E1E2"] = cmp
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

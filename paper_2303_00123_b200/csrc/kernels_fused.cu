@@ -355,6 +355,10 @@ bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t T, QcTmap* out, Pas
   if (std::popcount(xmask) > 4) return false;  // > 16 boxes per tile: keep the gather4 rows
   cuuint64_t gdim[5], gstride[4];
   cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < nd; ++i) {
+    const int end = i + 1 < nd ? start[i + 1] : nbits;
+    if (end - start[i] + (i == 0 && dbl ? 1 : 0) > 32) return false;  // tensor-map dims are <= 2^32
+  }
   for (int i = 0; i < 5; ++i) {
     if (i < nd) {
       const int end = i + 1 < nd ? start[i + 1] : nbits;
