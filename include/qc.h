@@ -126,7 +126,15 @@ typedef enum {
                                    (CUDA IPC handles all-gathered over NCCL) and one kernel
                                    per run swaps the two halves directly over NVLink (loads +
                                    stores, no staging copy); the pair splits each run in two
-                                   and brackets the kernel with a pairwise NCCL token barrier */
+                                   and brackets the kernel with a pairwise NCCL token barrier;
+                                 2: collective-fused pair passes -- a run of gates whose only
+                                   non-diagonal rank-bit qubit is g is planned over the local
+                                   bits + g; ranks r and r ^ 2^(g-n_loc) split every pass's
+                                   tiles, and a pass whose tile holds g moves the two tile
+                                   halves from / to both shards directly (TMA over the IPC-
+                                   mapped partner buffer): the exchange is fused into the
+                                   pass and the layout does not change (no swap back).  A
+                                   gate on two rank-bit qubits at once falls back to 1 */
 } qc_option;
 
 /* Counters of the most recent qc_run_circuit / qc_apply_gate. */
@@ -153,6 +161,9 @@ typedef struct qc_info {
     double last_flops_per_amp; /* fused runs: algorithmic flops per amplitude of the
                                   plan's fused ops (complex arithmetic counted;
                                   the ALU roofline numerator, qc_debug.h)      */
+    int64_t last_pair_segments; /* sharded runs with QC_OPT_EXCHANGE 2: pair segments
+                                   (gates on one rank-bit qubit run in place over
+                                   the pair's two shards, no exchange)          */
 } qc_info;
 
 /* Generic gate: any number of controls and a dense

@@ -53,6 +53,10 @@ qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, int* partner
  * with local bit l.  layout_out (n ints, may be NULL) = final layout. */
 qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
                                  int* steps, int max_steps, int* n_steps, int* layout_out);
+/* Same, for a QC_OPT_EXCHANGE mode (0/1: exchanges; 2: pair segments, kind 2
+ * = pair segment of `gates` gates on rank bit g, l = -1). */
+qc_status qc_debug_dist_schedule_ex(int n, int world, int relabel, int exchange_mode, const qc_gate* ops,
+                                    size_t n_ops, int* steps, int max_steps, int* n_steps, int* layout_out);
 
 /* Run one qubit-swap exchange of physical rank bit g with local bit l on a
  * sharded state (collective; enqueued on the state's stream); the layout is

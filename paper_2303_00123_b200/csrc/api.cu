@@ -309,7 +309,7 @@ uint64_t pass_tile_set(const PassDesc& d) {
 // ALU rate.  Rates from round-2 B200 measurements: TMA box
 // transport 4.1 / 4.55 / 5.3 / 5.7 TB/s when the tile's innermost run is 64 /
 // 128 / 256 / >= 512 B; gather4 rows 5.6 (1 KiB), 4.6 (512 B), 3.5 (less);
-// fused passes ~26 (c128) / ~45 (c64) algorithmic TFLOP/s.
+// fused passes ~34 (c128) / ~52 (c64) algorithmic TFLOP/s (after the full register frames).
 double plan_cost_model(const FusedPlan& fp, int n, bool dbl, bool box) {
   const double ab = dbl ? 16 : 8, N = std::ldexp(1.0, n);
   double t = 0;
@@ -326,7 +326,7 @@ double plan_cost_model(const FusedPlan& fp, int n, bool dbl, bool box) {
       const double row = ab * std::ldexp(1.0, d.rb);
       bw = row >= 1024 ? 5.6e12 : (row >= 512 ? 4.6e12 : 3.5e12);
     }
-    const double H = 2 * ab * N / bw, F = pass_flops_per_amp(pp) * N / (dbl ? 26e12 : 45e12);
+    const double H = 2 * ab * N / bw, F = pass_flops_per_amp(pp) * N / (dbl ? 34e12 : 52e12);
     t += std::sqrt(H * H + F * F);
   }
   return t;
@@ -372,9 +372,12 @@ FusedPlan plan_best(int n_plan, int k, int rb_default, int row_bits_opt, bool bo
 // controls / diagonal bits).  `tmap_base` / `tmap_bits`: the buffer and index
 // width the row tensor map spans.
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
-                            PlanEntry* e, void* tmap_base, int tmap_bits, bool remap) {
+                            PlanEntry* e, void* tmap_base, int tmap_bits, bool remap, uint64_t pair_mask,
+                            void* peer_base) {
   int k, rb, ctas;
-  plan_geometry(s, n_plan, &k, &rb, &ctas);
+  // pair segment: the pair's two ranks split every pass's tiles, so a pass
+  // needs >= 2 tiles (k < n_plan)
+  plan_geometry(s, pair_mask ? n_plan - 1 : n_plan, &k, &rb, &ctas);
   e->ctas = ctas;
   e->tile_bits = k;
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
@@ -387,23 +390,40 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   e->flops_per_amp = plan_flops_per_amp(fp);
   void* tb = tmap_base ? tmap_base : s->d;
   const int tbits = tmap_bits ? tmap_bits : n_plan;
-  const bool g4 = (s->tma_mode == 0 || s->tma_mode == 2) && make_row_tmap(tb, tbits, rb, s->dbl, &e->tmap);
+  const bool g4 = (s->tma_mode == 0 || s->tma_mode == 2) && make_row_tmap(tb, tbits, rb, s->dbl, &e->tmap) &&
+                  (!peer_base || make_row_tmap(peer_base, tbits, rb, s->dbl, &e->tmap_peer));
+  e->pair_mask = pair_mask;
   for (auto& p : fp.passes) {
     p.desc.g4 = g4 ? 1 : 0;
     p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
+    // pair segment: the pair bit never reaches an address (it selects the
+    // buffer); a pass whose tile holds it moves its two halves separately
+    p.desc.addr_strip = pair_mask;
+    p.desc.pair = (pass_tile_set(p.desc) & pair_mask) ? 1 : 0;
   }
   if (box) {
-    // one TMA box per tile where the tile's bit runs fit a 5-D tensor map
-    // (else that pass keeps the gather4 rows, or per-row copies)
+    // one TMA box per tile (per half tile of a pair pass) where the tile's bit
+    // runs fit a 5-D tensor map (else that pass keeps the gather4 rows, or
+    // per-row copies)
     e->tmaps.assign(fp.passes.size(), e->tmap);
+    if (peer_base) e->tmaps_peer.assign(fp.passes.size(), e->tmap_peer);
     for (size_t i = 0; i < fp.passes.size(); ++i) {
       PassDesc& d = fp.passes[i].desc;
-      if (make_box_tmap(tb, tbits, s->dbl, pass_tile_set(d), &e->tmaps[i], &d)) {
+      PassDesc d2 = d;
+      const uint64_t T = pass_tile_set(d) & ~pair_mask;
+      if (make_box_tmap(tb, tbits, s->dbl, T, &e->tmaps[i], &d2) &&
+          (!peer_base || make_box_tmap(peer_base, tbits, s->dbl, T, &e->tmaps_peer[i], &d2))) {
+        d = d2;
         d.g4 = 2;
         d.pshift = 31;
       }
     }
   }
+  for (auto& p : fp.passes)  // a gather4 request (4 rows) must not straddle a pair pass's two halves
+    if (p.desc.pair && p.desc.g4 == 1 && p.desc.k - p.desc.rb < 3) {
+      p.desc.g4 = 0;
+      p.desc.pshift = p.desc.rb;
+    }
   std::vector<uint8_t> blob = pack_plan(fp, s->dbl);
   for (auto& p : fp.passes) e->passes.push_back(p.desc);
   e->dbl = s->dbl;
@@ -468,6 +488,12 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   return QC_OK;
 }
 
+int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmap& tm,
+                const QcTmap& tm1, cudaStream_t st) {
+  return (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, tm, tm1, e->ctas, st)
+                             : launch_fused_pass(base, s->dbl, pd, e->d_blob, tm, tm1, e->ctas, st);
+}
+
 // Launch every pass of a fused entry; rank_bits / addr_bits: see PassDesc.
 int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
                   uint64_t addr_bits) {
@@ -476,8 +502,7 @@ int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64
     pd.rank_bits = rank_bits;
     pd.addr_bits = addr_bits;
     const QcTmap& tm = e->tmaps.empty() ? e->tmap : e->tmaps[i];
-    const int r = (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, tm, e->ctas, st)
-                                      : launch_fused_pass(base, s->dbl, pd, e->d_blob, tm, e->ctas, st);
+    const int r = launch_pass(s, e, i, pd, base, tm, tm, st);
     if (r) return r;
   }
   return 0;
@@ -994,7 +1019,7 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       break;
     case QC_OPT_REMAP: s->remap = v != 0; break;
     case QC_OPT_EXCHANGE:
-      if (v < 0 || v > 1) return fail(QC_ERR_INVALID_ARG, "exchange must be 0 (NCCL) or 1 (P2P)");
+      if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "exchange must be 0 (NCCL), 1 (P2P) or 2 (pair passes)");
       s->xmode = (int)v;
       break;
     case QC_OPT_JIT:
@@ -1028,6 +1053,7 @@ qc_status qc_get_info(const qc_state* s, qc_info* out) {
   out->n_local = s->dist ? s->n_loc : s->n;
   out->sharding = s->dist;
   out->last_exchanges = s->last_exchanges;
+  out->last_pair_segments = s->last_pair_segments;
   out->last_flops_per_amp = s->last_flops_per_amp;
   return QC_OK;
 }
@@ -1123,13 +1149,20 @@ extern "C" qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, i
 
 extern "C" qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
                                            int* steps, int max_steps, int* n_steps, int* layout_out) {
+  return qc_debug_dist_schedule_ex(n, world, relabel, 0, ops, n_ops, steps, max_steps, n_steps, layout_out);
+}
+
+extern "C" qc_status qc_debug_dist_schedule_ex(int n, int world, int relabel, int exchange_mode, const qc_gate* ops,
+                                              size_t n_ops, int* steps, int max_steps, int* n_steps,
+                                              int* layout_out) {
+  if (exchange_mode < 0 || exchange_mode > 2) return fail(QC_ERR_INVALID_ARG, "bad exchange mode");
   if (!n_steps || world < 2 || (world & (world - 1))) return fail(QC_ERR_INVALID_ARG, "bad arguments");
   for (size_t i = 0; i < n_ops; ++i) {
     const qc_status st = validate_gate(n, ops[i], i);
     if (st != QC_OK) return st;
   }
   std::vector<int> out, lay;
-  const qc_status st = dist_schedule_dry(n, world, relabel, ops, n_ops, out, lay);
+  const qc_status st = dist_schedule_dry(n, world, relabel, ops, n_ops, out, lay, nullptr, exchange_mode);
   if (st != QC_OK) return st;
   *n_steps = (int)out.size() / 4;
   if (steps) std::memcpy(steps, out.data(), sizeof(int) * std::min<size_t>(out.size(), (size_t)max_steps * 4));

@@ -43,12 +43,12 @@ struct DistPlan {
   std::vector<uint8_t> mkey;  // referenced generic gates' contents
   std::vector<int> layout_in, layout_out;
   struct Step {
-    int kind = 0;  // 0: fused local segment, 1: exchange
+    int kind = 0;  // 0: fused local segment, 1: exchange, 2: pair segment on rank bit g (QC_OPT_EXCHANGE 2)
     int g = -1, l = -1;
     std::unique_ptr<PlanEntry> seg;
   };
   std::vector<Step> steps;
-  int64_t exchanges = 0, relabels = 0, passes = 0;
+  int64_t exchanges = 0, relabels = 0, passes = 0, pair_segments = 0;
   int uses = 0;
 };
 
@@ -292,7 +292,7 @@ qc_status dist_exchange(qc_state* s, int g, int l) {
     }
     return QC_OK;
   }
-  if (s->xmode == 1) return p2p_exchange(s, g, l);
+  if (s->xmode >= 1) return p2p_exchange(s, g, l);  // (2: a gate needing two rank bits at once)
   // NCCL: send my runs to the partner, receive its runs into the same places.
   // Chunks alternate between two staging buffers: chunk i's send/recv runs on
   // the exchange stream while chunk i-1's copy into place runs on the state's
@@ -359,26 +359,49 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
     return it == uses[q].end() ? (long)1 << 40 : (long)*it;
   };
   std::vector<PGate> seg;
+  int seg_pair = -1;  // >= 0: the current segment is a pair segment on this rank bit
   auto flush = [&]() -> qc_status {
-    if (seg.empty()) return QC_OK;
+    if (seg.empty()) {
+      seg_pair = -1;
+      return QC_OK;
+    }
     DistPlan::Step st;
-    st.kind = 0;
+    st.kind = seg_pair >= 0 ? 2 : 0;
+    st.g = seg_pair;
     st.seg = std::make_unique<PlanEntry>();
     if (dry_run) {
       st.seg->fused_gates = (int64_t)seg.size();
       P->steps.push_back(std::move(st));
       seg.clear();
+      seg_pair = -1;
       return QC_OK;
     }
-    const uint64_t local_mask = (1ull << nl) - 1;
-    // remap on: the plan ends in the layout it started from (restore passes),
-    // so the exchange slot keeps the qubit the preceding SWAP2 put there
-    const qc_status r = build_fused_entry(s, seg, nl, local_mask, st.seg.get(), s->d,
-                                          s->dist == 1 ? n : nl, s->remap != 0);
+    qc_status r;
+    if (seg_pair < 0) {
+      const uint64_t local_mask = (1ull << nl) - 1;
+      // remap on: the plan ends in the layout it started from (restore passes),
+      // so the exchange slot keeps the qubit the preceding SWAP2 put there
+      r = build_fused_entry(s, seg, nl, local_mask, st.seg.get(), s->d, s->dist == 1 ? n : nl, s->remap != 0);
+    } else {
+      // pair segment: plan space = the nl local bits + the rank bit seg_pair
+      // relabelled to plan bit nl (the other rank bits stay constants)
+      for (PGate& pg : seg)
+        if (seg_pair != nl) pgate_swap_bits(pg, nl, seg_pair);
+      void* peer = nullptr;
+      if (s->dist == 2) {
+        r = ensure_peers(s);  // collective (same point of the schedule on every rank)
+        if (r != QC_OK) return r;
+        peer = s->peers[(size_t)(s->rank ^ (1 << (seg_pair - nl)))];
+      }
+      r = build_fused_entry(s, seg, nl + 1, (2ull << nl) - 1, st.seg.get(), s->d, s->dist == 1 ? n : nl,
+                            s->remap != 0, 1ull << nl, peer);
+    }
     if (r != QC_OK) return r;
     P->passes += (int64_t)st.seg->passes.size();
+    if (seg_pair >= 0) P->pair_segments++;
     P->steps.push_back(std::move(st));
     seg.clear();
+    seg_pair = -1;
     return QC_OK;
   };
   for (size_t i = 0; i < n_ops; ++i) {
@@ -391,6 +414,27 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       continue;
     }
     const uint64_t nd = op_nondiag_mask(op, mt);
+    if (s->xmode == 2) {
+      // pair passes: a gate with exactly one non-diagonal rank-bit qubit runs
+      // in a pair segment on that rank bit (no exchange, layout unchanged)
+      int gbit = -1, ng = 0;
+      for (int q = 0; q < n; ++q)
+        if ((nd & (1ull << q)) && lay[q] >= nl) {
+          gbit = lay[q];
+          ++ng;
+        }
+      if (ng == 1) {
+        if (seg_pair != gbit) {
+          if (seg_pair >= 0) {
+            qc_status r = flush();
+            if (r != QC_OK) return r;
+          }
+          seg_pair = gbit;  // a pending local segment joins the pair segment
+        }
+        seg.push_back(lower(op, lay, mt));
+        continue;
+      }
+    }
     uint64_t op_qubits = 0;
     {
       int qs[QC_MGATE_MAX_QUBITS];
@@ -447,9 +491,95 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
   return QC_OK;
 }
 
+// A pair segment (kind 2) on rank bit g: every pass is planned over the nl
+// local bits + the pair bit (plan bit nl).  The two ranks r, r ^ 2^(g-nl)
+// split each pass's tiles by the top tile-index bit (rank with pair bit v
+// takes half v).  A pass whose tile holds the pair bit reads and writes both
+// shards (its own and, over NVLink, the partner's: the collective is fused
+// into the pass -- no staging, no layout change); its tile halves come from
+// the two buffers.  Every other pass's half-v tiles lie in rank v's own
+// shard.  A pair pass is bracketed by pairwise barriers (the partner's
+// previous pass on its shard is done before, and its pair pass is done with
+// our shard after).  Loopback: all virtual ranks, pass by pass.
+qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
+  PlanEntry* e = st.seg.get();
+  const int nl = s->n_loc, j = st.g - nl;
+  const uint64_t pm = 1ull << nl;
+  struct Buf {
+    void* ptr;
+    uint64_t ab;
+    bool peer;
+  };
+  auto tmap_of = [&](const Buf& b, size_t i) -> const QcTmap& {
+    if (b.peer) return e->tmaps_peer.empty() ? e->tmap_peer : e->tmaps_peer[i];
+    return e->tmaps.empty() ? e->tmap : e->tmaps[i];
+  };
+  auto launch_rank = [&](int r, size_t i) -> int {
+    const int partner = r ^ (1 << j), v = (r >> j) & 1;
+    PassDesc pd = e->passes[i];
+    // rank bits in plan space: global bit g's value sits at plan bit nl (it is
+    // the pair bit, variable: not a constant) and global bit nl's at g
+    uint64_t R = (uint64_t)r << nl;
+    if (st.g != nl) {
+      const uint64_t bn = (R >> nl) & 1ull, bg = (R >> st.g) & 1ull;
+      R = (R & ~(pm | (1ull << st.g))) | (bn << st.g) | (bg << nl);
+    }
+    pd.rank_bits = R & ~pm;
+    const uint64_t half = pd.n_tiles / 2;
+    pd.n_tiles = half;
+    pd.tile0 = v ? half : 0;
+    Buf mine{s->d, 0, false}, peer{nullptr, 0, true};
+    if (s->dist == 1) {  // loopback: shards of one buffer, tensor maps over all n bits
+      mine.ab = (uint64_t)r << nl;
+      peer = Buf{s->d, (uint64_t)partner << nl, false};
+    } else {
+      peer.ptr = s->peers[(size_t)partner];
+    }
+    if (!pd.pair) {
+      pd.addr_bits = mine.ab;
+      const QcTmap& tm = tmap_of(mine, i);
+      return launch_pass(s, e, i, pd, mine.ptr, tm, tm, s->stream);
+    }
+    const Buf& h0 = v ? peer : mine;
+    const Buf& h1 = v ? mine : peer;
+    pd.addr_bits = h0.ab;
+    pd.addr_bits1 = h1.ab;
+    pd.state1 = (uint64_t)(uintptr_t)h1.ptr;
+    return launch_pass(s, e, i, pd, h0.ptr, tmap_of(h0, i), tmap_of(h1, i), s->stream);
+  };
+  const size_t np = e->passes.size();
+  if (s->dist == 1) {
+    for (size_t i = 0; i < np; ++i)
+      for (int r = 0; r < s->world; ++r)
+        if (const int rc = launch_rank(r, i)) return cuda_fail(s, rc, "pair segment pass (loopback)");
+    return QC_OK;
+  }
+  const int partner = s->rank ^ (1 << j);
+  bool prev_pair = false;
+  for (size_t i = 0; i < np; ++i) {
+    const bool pr = e->passes[i].pair != 0;
+    if (pr && !prev_pair) {
+      const qc_status b = pair_barrier(s, partner);
+      if (b != QC_OK) return b;
+    }
+    if (const int rc = launch_rank(s->rank, i)) return cuda_fail(s, rc, "pair segment pass");
+    if (pr) {
+      const qc_status b = pair_barrier(s, partner);
+      if (b != QC_OK) return b;
+    }
+    prev_pair = pr;
+  }
+  return QC_OK;
+}
+
 qc_status enqueue_dist(qc_state* s, DistPlan* P) {
   const uint64_t nloc_amps = 1ull << s->n_loc;
   for (auto& st : P->steps) {
+    if (st.kind == 2) {
+      const qc_status r = enqueue_pair_segment(s, st);
+      if (r != QC_OK) return r;
+      continue;
+    }
     if (st.kind == 1) {
       const qc_status r = dist_exchange(s, st.g, st.l);
       if (r != QC_OK) return r;
@@ -474,12 +604,13 @@ qc_status enqueue_dist(qc_state* s, DistPlan* P) {
 
 // Host-only schedule for tests (qc_debug.h): steps as (kind, g, l, gates).
 qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
-                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt) {
+                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt, int xmode) {
   qc_state s;
   s.n = n;
   s.world = world;
   s.n_loc = n - std::countr_zero((unsigned)world);
   s.relabel = relabel;
+  s.xmode = xmode;
   s.dist = 1;
   for (int q = 0; q < n; ++q) s.layout[q] = n - 1 - q;
   DistPlan P;
@@ -489,7 +620,7 @@ qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, s
     out.push_back(st.kind);
     out.push_back(st.g);
     out.push_back(st.l);
-    out.push_back(st.kind == 0 ? (int)st.seg->fused_gates : 0);
+    out.push_back(st.kind != 1 ? (int)st.seg->fused_gates : 0);
   }
   layout_out = P.layout_out;
   return QC_OK;
@@ -528,7 +659,7 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   }
   P->uses++;
   for (auto& st : P->steps) {
-    if (st.kind != 0) continue;
+    if (st.kind == 1) continue;
     st.seg->uses = P->uses;
     const qc_status r = maybe_jit(s, st.seg.get());
     if (r != QC_OK) return r;
@@ -539,7 +670,7 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   int64_t launches = 0;
   bool jit = true;
   for (auto& st : P->steps)
-    if (st.kind == 0) {
+    if (st.kind != 1) {
       launches += (int64_t)st.seg->passes.size() * (s->dist == 1 ? s->world : 1);
       jit = jit && st.seg->jit_state == 1;
     }
@@ -547,6 +678,7 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   s->last_launches = launches;
   s->last_relabels = P->relabels;
   s->last_exchanges = P->exchanges;
+  s->last_pair_segments = P->pair_segments;
   s->last_graph = 0;
   s->last_jit = jit ? 1 : 0;
   return QC_OK;

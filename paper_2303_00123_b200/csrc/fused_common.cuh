@@ -398,9 +398,14 @@ __device__ __forceinline__ void qc_prun_slot(C (&v)[kSlots], const C w0, const C
 //   void setup(unsigned char* extra, const PassDesc&)   all threads, before sync
 //   void prologue(uint64_t tbase, int par)             compute threads, per tile
 //   void tile(C* buf, uint64_t tbase, int par)          compute threads, per tile
+// Tile transport of a pair pass (pd.pair): the top tile-local bit is the
+// pair bit, so the tile's lower half (pair bit 0) and upper half (pair bit 1)
+// are moved separately, each from / to its own buffer (tmap / tmap1, state /
+// state1, addr_bits / addr_bits1); every other pass has one half.
 template <typename C, int NBUF, class Body>
 __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const PassDesc& pd,
-                                                  const QcTmap* tmap, unsigned char* smem_raw, Body& body) {
+                                                  const QcTmap* tmap, const QcTmap* tmap1, unsigned char* smem_raw,
+                                                  Body& body) {
   const int rb = pd.rb, k = pd.k, ps = pd.pshift;
   const uint32_t PAD = kPadBytes / sizeof(C);
   const uint32_t row_amps = 1u << rb;
@@ -423,7 +428,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   for (uint32_t r = tid; r < nrows; r += blockDim.x) {
     uint64_t g = 0;
     for (int j = 0; j < pd.n_hi; ++j) g |= (uint64_t)((r >> j) & 1u) << pd.hi_pos[j];
-    row_off[r] = g;
+    row_off[r] = g & ~pd.addr_strip;
   }
   if (tid == 0) {
     for (int b = 0; b < NBUF; ++b) {
@@ -453,35 +458,44 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
       if (i >= NBUF) {  // buffer b holds finished tile i-NBUF: write it back
         const uint64_t ip = i - NBUF;
         qc_mbar_wait(&empty[b], (uint32_t)((ip / NBUF) & 1ull));
-        const uint64_t base = qc_tile_base(pd, blockIdx.x + ip * gridDim.x) | pd.addr_bits;
+        const uint64_t base = qc_tile_base(pd, pd.tile0 + blockIdx.x + ip * gridDim.x) & ~pd.addr_strip;
         if (pd.g4 == 2) {
           if (lane == 0) {
-            int32_t c[5];
-            qc_box_coords<C>(pd, base, c);
-            const int32_t c4 = c[4];
-            uint32_t v = 0, j = 0;
-            do {  // every combination of the extra tile bits (one box if none)
-              c[4] = c4 | (int32_t)v;
-              qc_box_store(tmap, c, buf + ((size_t)j << pd.bx_sub));
-              v = (v - pd.bx_xmask) & pd.bx_xmask;
-              ++j;
-            } while (v);
+            for (int h = 0; h <= pd.pair; ++h) {
+              int32_t c[5];
+              qc_box_coords<C>(pd, base | (h ? pd.addr_bits1 : pd.addr_bits), c);
+              const int32_t c4 = c[4];
+              C* hb = buf + ((size_t)h << (k - 1));
+              uint32_t v = 0, j = 0;
+              do {  // every combination of the extra tile bits (one box if none)
+                c[4] = c4 | (int32_t)v;
+                qc_box_store(h ? tmap1 : tmap, c, hb + ((size_t)j << pd.bx_sub));
+                v = (v - pd.bx_xmask) & pd.bx_xmask;
+                ++j;
+              } while (v);
+            }
           }
         } else if (pd.g4) {
-          for (uint32_t r = 4 * lane; r < nrows; r += 128)
-            qc_scatter4(tmap, (int32_t)((base | row_off[r]) >> rb), (int32_t)((base | row_off[r + 1]) >> rb),
-                        (int32_t)((base | row_off[r + 2]) >> rb), (int32_t)((base | row_off[r + 3]) >> rb),
+          for (uint32_t r = 4 * lane; r < nrows; r += 128) {
+            const bool h = pd.pair && r >= nrows / 2;
+            const uint64_t bb = base | (h ? pd.addr_bits1 : pd.addr_bits);
+            qc_scatter4(h ? tmap1 : tmap, (int32_t)((bb | row_off[r]) >> rb), (int32_t)((bb | row_off[r + 1]) >> rb),
+                        (int32_t)((bb | row_off[r + 2]) >> rb), (int32_t)((bb | row_off[r + 3]) >> rb),
                         buf + row_at(r));
+          }
         } else {
-          for (uint32_t r = lane; r < nrows; r += 32)
-            qc_bulk_s2g(state + (base | row_off[r]), buf + row_at(r), row_bytes);
+          for (uint32_t r = lane; r < nrows; r += 32) {
+            const bool h = pd.pair && r >= nrows / 2;
+            C* st = h ? reinterpret_cast<C*>(pd.state1) : state;
+            qc_bulk_s2g(st + (base | (h ? pd.addr_bits1 : pd.addr_bits) | row_off[r]), buf + row_at(r), row_bytes);
+          }
         }
         qc_bulk_commit();
         qc_bulk_wait_read0();  // smem of buffer b may be overwritten after this
         __syncwarp();
       }
       if (i < my_n) {
-        const uint64_t base = qc_tile_base(pd, blockIdx.x + i * gridDim.x) | pd.addr_bits;
+        const uint64_t base = qc_tile_base(pd, pd.tile0 + blockIdx.x + i * gridDim.x) & ~pd.addr_strip;
         if (lane == 0) {
           // full[b]'s pending phase now belongs to tile i (atomic: the tag is
           // polled by the consumer groups -- an explicit flag, not a data race)
@@ -491,25 +505,35 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
         __syncwarp();
         if (pd.g4 == 2) {
           if (lane == 0) {
-            int32_t c[5];
-            qc_box_coords<C>(pd, base, c);
-            const int32_t c4 = c[4];
-            uint32_t v = 0, j = 0;
-            do {
-              c[4] = c4 | (int32_t)v;
-              qc_box_load(buf + ((size_t)j << pd.bx_sub), tmap, c, &full[b]);
-              v = (v - pd.bx_xmask) & pd.bx_xmask;
-              ++j;
-            } while (v);
+            for (int h = 0; h <= pd.pair; ++h) {
+              int32_t c[5];
+              qc_box_coords<C>(pd, base | (h ? pd.addr_bits1 : pd.addr_bits), c);
+              const int32_t c4 = c[4];
+              C* hb = buf + ((size_t)h << (k - 1));
+              uint32_t v = 0, j = 0;
+              do {
+                c[4] = c4 | (int32_t)v;
+                qc_box_load(hb + ((size_t)j << pd.bx_sub), h ? tmap1 : tmap, c, &full[b]);
+                v = (v - pd.bx_xmask) & pd.bx_xmask;
+                ++j;
+              } while (v);
+            }
           }
         } else if (pd.g4) {
-          for (uint32_t r = 4 * lane; r < nrows; r += 128)
-            qc_gather4(buf + row_at(r), tmap, (int32_t)((base | row_off[r]) >> rb),
-                       (int32_t)((base | row_off[r + 1]) >> rb), (int32_t)((base | row_off[r + 2]) >> rb),
-                       (int32_t)((base | row_off[r + 3]) >> rb), &full[b]);
+          for (uint32_t r = 4 * lane; r < nrows; r += 128) {
+            const bool h = pd.pair && r >= nrows / 2;
+            const uint64_t bb = base | (h ? pd.addr_bits1 : pd.addr_bits);
+            qc_gather4(buf + row_at(r), h ? tmap1 : tmap, (int32_t)((bb | row_off[r]) >> rb),
+                       (int32_t)((bb | row_off[r + 1]) >> rb), (int32_t)((bb | row_off[r + 2]) >> rb),
+                       (int32_t)((bb | row_off[r + 3]) >> rb), &full[b]);
+          }
         } else {
-          for (uint32_t r = lane; r < nrows; r += 32)
-            qc_bulk_g2s(buf + row_at(r), state + (base | row_off[r]), row_bytes, &full[b]);
+          for (uint32_t r = lane; r < nrows; r += 32) {
+            const bool h = pd.pair && r >= nrows / 2;
+            const C* st = h ? reinterpret_cast<const C*>(pd.state1) : state;
+            qc_bulk_g2s(buf + row_at(r), st + (base | (h ? pd.addr_bits1 : pd.addr_bits) | row_off[r]), row_bytes,
+                        &full[b]);
+          }
         }
       }
     }
@@ -525,7 +549,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     const int par = (int)(i % kWSlots);
     // global index of the tile's first amplitude (rank bits included): used
     // for control predicates and diagonal bits; memory addresses stay local
-    const uint64_t tbase = qc_tile_base(pd, blockIdx.x + i * gridDim.x) | pd.rank_bits;
+    const uint64_t tbase = qc_tile_base(pd, pd.tile0 + blockIdx.x + i * gridDim.x) | pd.rank_bits;
     body.prologue(tbase, par);
     if (kGroups > 1 && NBUF % kGroups) {
       // wait until the producer has claimed buffer b for this tile (see fused_types.h)

@@ -98,6 +98,18 @@ struct PassDesc {
   uint64_t rank_bits;     // sharded state: this rank's global bits (rank << n_loc), OR-ed
                           // into every tile's base for predicates / diagonal bits only
   uint64_t addr_bits;     // OR-ed into amplitude addresses (loopback: shards share one buffer)
+  // Pair segments of a sharded state (QC_OPT_EXCHANGE 2, dist.cu): the plan
+  // spans the n_loc local bits plus ONE rank bit, placed at plan bit n_loc
+  // (the "pair bit"); the two ranks that differ in it split every pass's
+  // tiles in half.
+  uint64_t tile0;         // first tile index of this launch (n_tiles = tiles of this launch)
+  uint64_t addr_strip;    // plan bits cleared from tile bases / row offsets before addressing
+  uint64_t addr_bits1;    // pair == 1: addr_bits of the pair-bit-1 half of every tile
+  uint64_t state1;        // pair == 1: buffer holding the pair-bit-1 half (per-row copy transport)
+  int32_t pair;           // 1: the tile's top local bit is the pair bit -- its two halves live
+                          // in two buffers (tmap / state / addr_bits and tmap1 / state1 /
+                          // addr_bits1: the ranks' own shard and its partner's, over NVLink)
+  int32_t pad1_;
 };
 
 }  // namespace qc

@@ -580,6 +580,12 @@ void emit_pass(int n, int k, int rb, uint64_t T, const std::vector<Group>& group
   d.g4 = 0;
   d.rank_bits = 0;
   d.addr_bits = 0;
+  d.tile0 = 0;
+  d.addr_strip = 0;
+  d.addr_bits1 = 0;
+  d.state1 = 0;
+  d.pair = 0;
+  d.pad1_ = 0;
   d.n_hi = 0;
   for (int p = rb; p < n; ++p)
     if (T & (1ull << p)) d.hi_pos[d.n_hi++] = p;
@@ -976,5 +982,8 @@ std::vector<uint8_t> pack_plan(FusedPlan& plan, bool dbl) {
   }
   return blob;
 }
+
+// Exported for dist.cu (pair segments relabel a rank bit into plan bit n_loc).
+void pgate_swap_bits(PGate& g, int a, int b) { swap_bits(g, a, b); }
 
 }  // namespace qc

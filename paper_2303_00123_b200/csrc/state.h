@@ -24,6 +24,10 @@ struct PlanEntry {
   int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
   QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
   std::vector<QcTmap> tmaps;         // per-pass box tensor maps (PassDesc g4 == 2; empty otherwise)
+  // pair segments (dist.cu, QC_OPT_EXCHANGE 2): plan bit n_loc is a rank bit
+  uint64_t pair_mask = 0;            // the pair bit (plan space); 0: not a pair segment
+  QcTmap tmap_peer{};                // the partner's buffer (P2P): row tensor map ...
+  std::vector<QcTmap> tmaps_peer;    // ... and per-pass box tensor maps
   bool dbl = true;
   int64_t relabels = 0;
   int uses = 0;
@@ -66,9 +70,13 @@ PGate lower(const qc_gate& g, const int* layout, const MTable* mt = nullptr);
 qc_status validate_gate(int n, const qc_gate& g, size_t idx, const MTable* mt = nullptr);
 uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt);
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
-                            PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0, bool remap = false);
+                            PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0, bool remap = false,
+                            uint64_t pair_mask = 0, void* peer_base = nullptr);
 int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
                   uint64_t addr_bits);
+// One pass of an entry with explicit buffers (pair segments: halves in two buffers).
+int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmap& tm,
+                const QcTmap& tm1, cudaStream_t st);
 qc_status maybe_jit(qc_state* s, PlanEntry* e);
 qc_status ensure_fused_configured(qc_state* s);
 extern const int kArity[16];
@@ -84,7 +92,8 @@ qc_status nccl_allreduce_sum(qc_state* s, double* host_value);
 void nccl_destroy(qc_state* s);
 void dist_release(qc_state* s);  // drop sharded plans + communicator
 qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
-                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt = nullptr);
+                            std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt = nullptr,
+                            int xmode = 0);
 struct ExchangeRun {
   uint64_t offset;  // amplitudes, within the shard
   uint64_t count;
@@ -130,12 +139,13 @@ struct qc_state {
   void* nccl_comm = nullptr;
   void* d_xstage = nullptr;          // exchange staging: two chunks (ping-pong)
   size_t xstage_bytes = 0;
-  int xmode = 0;                     // QC_OPT_EXCHANGE: 0 NCCL send/recv, 1 P2P swap kernel
+  int xmode = 0;                     // QC_OPT_EXCHANGE: 0 NCCL send/recv, 1 P2P swap kernel, 2 pair passes
   cudaStream_t xstream = nullptr;    // NCCL exchange stream (copies stay on `stream`)
   cudaEvent_t xev[5] = {};           // start, recv_done[2], copy_done[2]
   std::vector<void*> peers;          // P2P: every rank's state buffer, IPC-mapped (own: d)
   int* d_token = nullptr;            // P2P: pairwise barrier token (2 ints)
   int64_t last_exchanges = 0;
+  int64_t last_pair_segments = 0;
   qc::DistCache* dcache = nullptr;  // sharded plans (owned by dist.cu)
   ~qc_state();
 };

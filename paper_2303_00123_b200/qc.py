@@ -73,7 +73,7 @@ class qc_info(ctypes.Structure):
                 ("last_blocks", ctypes.c_int64), ("last_jit", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("n_local", ctypes.c_int32),
                 ("sharding", ctypes.c_int32), ("last_exchanges", ctypes.c_int64),
-                ("last_flops_per_amp", ctypes.c_double)]
+                ("last_flops_per_amp", ctypes.c_double), ("last_pair_segments", ctypes.c_int64)]
 
 
 class qc_plan_stats(ctypes.Structure):
@@ -86,7 +86,7 @@ class qc_plan_stats(ctypes.Structure):
                 ("swz_substages", ctypes.c_int64)]
 
 
-DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_exchange",
+DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_dist_schedule_ex", "qc_debug_exchange",
                  "qc_debug_fma_peak", "qc_debug_box_layout"]
 
 _lib = None
@@ -131,6 +131,8 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_exchange_runs.restype = ctypes.c_int
     L.qc_debug_dist_schedule.argtypes = [i32, i32, i32, vp, sz, vp, i32, ctypes.POINTER(ctypes.c_int), vp]
     L.qc_debug_dist_schedule.restype = ctypes.c_int
+    L.qc_debug_dist_schedule_ex.argtypes = [i32, i32, i32, i32, vp, sz, vp, i32, ctypes.POINTER(ctypes.c_int), vp]
+    L.qc_debug_dist_schedule_ex.restype = ctypes.c_int
     L.qc_debug_exchange.argtypes = [vp, i32, i32]
     L.qc_debug_exchange.restype = ctypes.c_int
     L.qc_debug_box_layout.argtypes = [u64, i32, i32, ctypes.POINTER(ctypes.c_int), vp, vp,
@@ -371,7 +373,8 @@ class State:
                 "last_graph": bool(i.last_graph), "tile_bits": i.tile_bits,
                 "last_blocks": i.last_blocks, "last_jit": bool(i.last_jit), "world": i.world,
                 "rank": i.rank, "n_local": i.n_local, "sharding": i.sharding,
-                "last_exchanges": i.last_exchanges, "last_flops_per_amp": i.last_flops_per_amp}
+                "last_exchanges": i.last_exchanges, "last_flops_per_amp": i.last_flops_per_amp,
+                "last_pair_segments": i.last_pair_segments}
 
     @property
     def stream(self) -> int:
@@ -435,15 +438,16 @@ def debug_exchange_runs(n_loc: int, rank: int, g: int, l: int):
     return partner.value, [(int(offs[i]), int(cnts[i])) for i in range(min(nr.value, cap))]
 
 
-def debug_dist_schedule(n: int, world: int, ops, relabel: bool = True):
-    """Host-only sharded schedule: ([(kind, g, l, gates)], final layout)."""
+def debug_dist_schedule(n: int, world: int, ops, relabel: bool = True, exchange: int = 0):
+    """Host-only sharded schedule: ([(kind, g, l, gates)], final layout); kind 0
+    local segment, 1 exchange, 2 pair segment (exchange mode 2)."""
     arr = ops if isinstance(ops, np.ndarray) else encode_ops(ops)
     arr = np.ascontiguousarray(arr)
     cap = 1 << 14
     steps = np.zeros(4 * cap, dtype=np.int32)
     lay = np.zeros(64, dtype=np.int32)
     ns = ctypes.c_int()
-    _check(lib().qc_debug_dist_schedule(n, world, int(relabel), arr.ctypes.data if len(arr) else None,
+    _check(lib().qc_debug_dist_schedule_ex(n, world, int(relabel), int(exchange), arr.ctypes.data if len(arr) else None,
                                         len(arr), steps.ctypes.data, cap, ctypes.byref(ns), lay.ctypes.data))
     out = [tuple(int(x) for x in steps[4 * i:4 * i + 4]) for i in range(min(ns.value, cap))]
     return out, [int(x) for x in lay[:n]]

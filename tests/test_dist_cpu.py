@@ -142,3 +142,40 @@ def test_schedule_exchange_counts_at_full_size():
     assert count(36, 8, qcgen.qft(36)) == 4
     assert count(33, 8, qcgen.tfxy(33, 10)) == 51
     assert count(35, 4, qcgen.tfxy(35, 10)) == 31
+
+
+def test_pair_segment_schedule():
+    """QC_OPT_EXCHANGE 2: a run of gates whose only non-diagonal rank-bit
+    qubit is g becomes one pair segment on g (no exchange, layout unchanged);
+    a gate needing two rank bits at once falls back to exchanges."""
+    def steps_of(n, world, ops):
+        steps, lay = qc.debug_dist_schedule(n, world, ops, exchange=2)
+        return steps, lay
+
+    def relabelled(n, ops):  # canonical layout after the SWAP relabels only
+        lay = [n - 1 - q for q in range(n)]
+        for op in ops:
+            if op.name == "SWAP":
+                a, b = op.qubits
+                lay[a], lay[b] = lay[b], lay[a]
+        return lay
+    n, world = 36, 8
+    steps, lay = steps_of(n, world, qcgen.qft(n))
+    assert [(k, g) for k, g, _, _ in steps] == [(2, 35), (2, 34), (2, 33)]
+    assert lay == relabelled(n, qcgen.qft(n))
+    assert sum(s[3] for s in steps) == sum(1 for op in qcgen.qft(n) if op.name != "SWAP")
+    for n, world in ((33, 8), (35, 4), (16, 4)):
+        ops = qcgen.tfxy(n, 4)
+        steps, lay = steps_of(n, world, ops)
+        assert all(k in (0, 2) for k, _, _, _ in steps) and any(k == 2 for k, _, _, _ in steps)
+        assert lay == [n - 1 - q for q in range(n)]
+        assert sum(s[3] for s in steps) == len(ops)
+        p = world.bit_length() - 1
+        assert all(n - p <= g < n for k, g, _, _ in steps if k == 2)
+    # a dense 2-qubit gate on two rank-bit qubits: exchanges bring both local
+    u = qcgen.random_unitary(4, np.random.default_rng(0))
+    steps, lay = steps_of(14, 4, [qcgen.Op("U2", (0, 1), matrix=u)])
+    assert [s[0] for s in steps].count(1) == 2 and sorted(lay) == list(range(14))
+    # gates on local qubits only: one local segment
+    steps, _ = steps_of(14, 4, [qcgen.Op("H", (q,)) for q in range(2, 14)])
+    assert [s[0] for s in steps] == [0]

@@ -106,3 +106,45 @@ def test_loopback_global_controls_and_diagonals(qcmod):
     got, info = run_lb(qcmod, n, "c128", world, ops)
     assert info["last_exchanges"] == 0
     assert maxerr(got, ref(n, "c128", ops)) <= 1e-12
+
+
+# ---- collective-fused pair passes (QC_OPT_EXCHANGE 2): gates on one rank-bit
+# qubit run in place over the pair's two shards (tile halves from both), no
+# exchange.  Loopback: the two halves come from two shards of one buffer
+# through the same PassDesc fields (tile0 / addr_strip / addr_bits1 / state1 /
+# second tensor map) the NCCL path fills with the IPC-mapped partner buffer.
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("world,n", [(2, 13), (4, 14), (8, 16)])
+def test_pair_passes_random_circuits(qcmod, prec, world, n):
+    ops = qcgen.random_circuit(n, 150, seed=70 + n + world)
+    got, info = run_lb(qcmod, n, prec, world, ops, exchange=2)
+    assert info["last_pair_segments"] > 0
+    assert maxerr(got, ref(n, prec, ops)) <= TOL[prec]
+
+
+@pytest.mark.parametrize("world,n", [(2, 14), (4, 16), (8, 18)])
+def test_pair_passes_qft_tfxy(qcmod, world, n):
+    for ops in (qcgen.qft(n), qcgen.tfxy(n, 3)):
+        got, info = run_lb(qcmod, n, "c128", world, ops, exchange=2)
+        assert info["last_pair_segments"] > 0 and info["last_exchanges"] == 0
+        assert maxerr(got, ref(n, "c128", ops)) <= 1e-12
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(tma_mode=2), dict(tma_mode=1), dict(row_bits=6),
+                                  dict(remap=0), dict(jit=0)])
+def test_pair_passes_transports(qcmod, opts):
+    """Every tile transport (box halves, gather4 rows, per-row copies) and the
+    AOT / JIT kernels on pair passes; the layout is unchanged afterwards."""
+    n, world = 15, 4
+    ops = qcgen.qft(n) + qcgen.random_circuit(n, 80, seed=12)
+    got, info = run_lb(qcmod, n, "c128", world, ops, reps=2, exchange=2, **opts)
+    assert info["last_pair_segments"] > 0
+    assert maxerr(got, ref(n, "c128", ops, reps=2)) <= 1e-12
+
+
+def test_pair_passes_permutation_bit_exact(qcmod):
+    n, world = 14, 4
+    ops = qcgen.random_circuit(n, 200, seed=19, kinds=("X", "CNOT", "SWAP", "CCX"))
+    got, info = run_lb(qcmod, n, "c128", world, ops, exchange=2)
+    assert info["last_pair_segments"] > 0
+    assert np.array_equal(got, ref(n, "c128", ops))

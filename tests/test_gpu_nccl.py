@@ -1,7 +1,8 @@
 """NCCL-sharded states across >= 2 GPUs, one process per GPU:
 every rank's canonical shard after QFT / TFXY / random (incl. generic) circuits
-vs the CPU oracle, for both exchange backends (QC_OPT_EXCHANGE 0: NCCL
-send/recv with ping-pong staging, 1: P2P swap kernel over CUDA IPC), and
+vs the CPU oracle, for every exchange backend (QC_OPT_EXCHANGE 0: NCCL
+send/recv with ping-pong staging, 1: P2P swap kernel over CUDA IPC, 2: pair
+passes reading / writing the partner's shard over the IPC mapping), and
 qc_state_init_basis on a shard.  Skipped on boxes with one GPU (the loopback
 backend in test_gpu_dist.py covers the same schedule on one GPU)."""
 import numpy as np
@@ -44,7 +45,7 @@ def _worker(rank, world, uid, n, prec, kind, xmode, q):
             s.init_random(qcgen.STATE_SEED)
             s.run(ops)
             s.run(ops)  # second run: JIT kernels, cached sharded plan
-            ex = s.info()["last_exchanges"]
+            ex = s.info()["last_exchanges"] + s.info()["last_pair_segments"]
             s.canonicalize()
             got = s.read(rank << nl, 1 << nl)
             # init_basis on a shard: one unit amplitude, on the owning rank only
@@ -72,7 +73,7 @@ def _run(world, n, prec, kind, xmode):
 
 
 @need2
-@pytest.mark.parametrize("xmode", [0, 1])
+@pytest.mark.parametrize("xmode", [0, 1, 2])
 @pytest.mark.parametrize("kind,prec", [("qft", "c128"), ("tfxy", "c128"), ("random", "c128"), ("qft", "c64")])
 def test_nccl_shards_match_oracle(kind, prec, xmode):
     world = 2
