@@ -50,7 +50,9 @@ qc_status qc_debug_exchange_runs(int n_loc, int rank, int g, int l, int* partner
 /* The sharded schedule qc_run_circuit would execute from the canonical
  * layout (host only, deterministic): steps[4*i..] = (kind, g, l, gates) with
  * kind 0 = fused local segment of `gates` gates, 1 = exchange of rank bit g
- * with local bit l.  layout_out (n ints, may be NULL) = final layout. */
+ * with local bit l (gates = 1: one of the exchanges at the end that return
+ * the layout to the one the SWAP relabels alone give).  layout_out (n ints,
+ * may be NULL) = final layout. */
 qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
                                  int* steps, int max_steps, int* n_steps, int* layout_out);
 /* Same, for a QC_OPT_EXCHANGE mode (0/1: exchanges; 2: pair segments, kind 2

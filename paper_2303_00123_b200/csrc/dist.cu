@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <bit>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -45,10 +46,12 @@ struct DistPlan {
   struct Step {
     int kind = 0;  // 0: fused local segment, 1: exchange, 2: pair segment on rank bit g (QC_OPT_EXCHANGE 2)
     int g = -1, l = -1;
+    bool restore = false;  // exchange that undoes the schedule's permutation at the end
     std::unique_ptr<PlanEntry> seg;
   };
   std::vector<Step> steps;
   int64_t exchanges = 0, relabels = 0, passes = 0, pair_segments = 0;
+  int64_t restore_exchanges = 0;  // of `exchanges`: undoing the schedule's permutation at the end
   int uses = 0;
 };
 
@@ -343,8 +346,9 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
                           bool dry_run = false) {
   const int n = s->n, nl = s->n_loc;
   const int L = nl - 1;  // exchange slot: the top local bit (one contiguous half per direction)
-  int lay[64], inv[64];
+  int lay[64], inv[64], rel[64];
   std::memcpy(lay, s->layout, sizeof(int) * n);
+  std::memcpy(rel, s->layout, sizeof(int) * n);  // the layout after the SWAP relabels only
   for (int q = 0; q < n; ++q) inv[lay[q]] = q;
   // next non-diagonal use of each logical qubit after op i (Belady)
   std::vector<std::vector<int>> uses(n);
@@ -408,6 +412,7 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
     const qc_gate& op = ops[i];
     if (op.op == QC_SWAP && s->relabel) {
       std::swap(lay[op.qubits[0]], lay[op.qubits[1]]);
+      std::swap(rel[op.qubits[0]], rel[op.qubits[1]]);
       inv[lay[op.qubits[0]]] = op.qubits[0];
       inv[lay[op.qubits[1]]] = op.qubits[1];
       P->relabels++;
@@ -485,6 +490,59 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
     PGate pg = lower(op, lay, mt);
     seg.push_back(pg);
   }
+  // Restore: undo the exchanges' permutation so the run ends in the layout
+  // the SWAP relabels alone give (so a repeated circuit starts from a layout
+  // it has seen: its sharded plan, JIT kernels and timing are reused instead
+  // of re-planned every run).  Rank bits first -- the qubit each should hold
+  // is brought to the exchange slot L (a local SWAP2 fused into the last
+  // segment, or an exchange if it sits on another rank bit) and exchanged
+  // into place -- then the local bits by SWAP2s in the last segment.
+  auto swap_local = [&](int a, int b) {  // physical SWAP of two local bits
+    if (a == b) return;
+    PGate sw;
+    sw.kind = GK::SWAP2;
+    sw.t0 = std::max(a, b);
+    sw.t1 = std::min(a, b);
+    seg.push_back(sw);
+    const int qa = inv[a], qb = inv[b];
+    std::swap(lay[qa], lay[qb]);
+    inv[lay[qa]] = qa;
+    inv[lay[qb]] = qb;
+  };
+  auto exchange = [&](int g) -> qc_status {  // rank bit g <-> L
+    qc_status fr = flush();
+    if (fr != QC_OK) return fr;
+    DistPlan::Step ex;
+    ex.kind = 1;
+    ex.g = g;
+    ex.l = L;
+    ex.restore = true;
+    P->steps.push_back(std::move(ex));
+    P->exchanges++;
+    P->restore_exchanges++;
+    const int qg = inv[g], ql = inv[L];
+    std::swap(lay[qg], lay[ql]);
+    inv[lay[qg]] = qg;
+    inv[lay[ql]] = ql;
+    return QC_OK;
+  };
+  static const bool restore = !getenv("QC_DIST_RESTORE") || atoi(getenv("QC_DIST_RESTORE")) != 0;
+  int rinv[64];
+  for (int q = 0; q < n; ++q) rinv[rel[q]] = q;
+  for (int g = nl; g < n && restore; ++g) {
+    const int want = rinv[g];
+    if (inv[g] == want) continue;
+    if (lay[want] >= nl) {  // on a later rank bit: bring it to L first
+      qc_status er = exchange(lay[want]);
+      if (er != QC_OK) return er;
+    } else {
+      swap_local(lay[want], L);
+    }
+    qc_status er = exchange(g);
+    if (er != QC_OK) return er;
+  }
+  for (int p = 0; p < nl && restore; ++p)
+    if (inv[p] != rinv[p]) swap_local(p, lay[rinv[p]]);
   qc_status r = flush();
   if (r != QC_OK) return r;
   P->layout_out.assign(lay, lay + n);
@@ -620,7 +678,7 @@ qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, s
     out.push_back(st.kind);
     out.push_back(st.g);
     out.push_back(st.l);
-    out.push_back(st.kind != 1 ? (int)st.seg->fused_gates : 0);
+    out.push_back(st.kind != 1 ? (int)st.seg->fused_gates : (st.restore ? 1 : 0));
   }
   layout_out = P.layout_out;
   return QC_OK;
@@ -634,7 +692,7 @@ qc_status run_dist(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   const uint64_t salt = 0xd157ull ^ ((uint64_t)s->relabel << 2) ^ ((uint64_t)s->block_fusion << 3) ^
                         ((uint64_t)s->tile_bits << 8) ^ ((uint64_t)s->row_bits << 16) ^
                         ((uint64_t)s->tma_mode << 24) ^ ((uint64_t)s->jit << 28) ^ ((uint64_t)s->remap << 32) ^
-                        ((uint64_t)s->ctas << 36) ^ ((uint64_t)s->fusion << 56);
+                        ((uint64_t)s->ctas << 36) ^ ((uint64_t)s->xmode << 44) ^ ((uint64_t)s->fusion << 56);
   std::vector<uint8_t> mkey = mtable_key(ops, n_ops, mt);
   uint64_t key = hash_ops(ops, n_ops, s->layout, s->n, salt);
   for (uint8_t b : mkey) key = (key ^ b) * 0x100000001b3ull;

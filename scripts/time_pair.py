@@ -6,7 +6,7 @@ rates need >= 2 GPUs.
 
   python scripts/time_pair.py qft:30:2 tfxy:28:2 ...   (family:n:world)
 """
-import os, sys
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import qcgen
@@ -23,15 +23,18 @@ for w in sys.argv[1:]:
             s.init_random(1)
             st = torch.cuda.ExternalStream(s.stream)
             with torch.cuda.stream(st):
-                for _ in range(3):
+                for _ in range(6):  # 2 layouts (SWAP relabels) x (plan, JIT, warm)
                     s.run(arr)
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(st)
-                for _ in range(3):
+                h0 = time.perf_counter()
+                for _ in range(4):
                     s.run(arr)
+                h1 = time.perf_counter()
                 b.record(st)
                 torch.cuda.synchronize()
             i = s.info()
-            print(f"{w} exchange={xm}: {a.elapsed_time(b) / 3:.2f} ms, passes {i['last_passes']}, "
-                  f"exchanges {i['last_exchanges']}, pair segments {i['last_pair_segments']}", flush=True)
+            print(f"{w} exchange={xm}: {a.elapsed_time(b) / 4:.2f} ms, passes {i['last_passes']}, "
+                  f"exchanges {i['last_exchanges']}, pair segments {i['last_pair_segments']}, "
+                  f"host enqueue {(h1 - h0) / 4 * 1e3:.2f} ms/run, jit {i['last_jit']}", flush=True)

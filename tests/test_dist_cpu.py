@@ -127,8 +127,10 @@ def test_schedule_64bit_qubit_masks(n, world):
     for gq in range(p):
         steps, _ = qc.debug_dist_schedule(n, world, [qcgen.Op("H", (33 if n > 33 else n - 1,)),
                                                      qcgen.Op("H", (gq,))])
-        ex = [s for s in steps if s[0] == 1]
+        ex = [s for s in steps if s[0] == 1 and s[3] == 0]
         assert len(ex) == 1 and ex[0][1] == n - 1 - gq and ex[0][2] == n - p - 1
+        back = [s for s in steps if s[0] == 1 and s[3] == 1]  # the restore: the same exchange again
+        assert back == [(1, n - 1 - gq, n - p - 1, 1)]
 
 
 def test_schedule_exchange_counts_at_full_size():
@@ -138,7 +140,11 @@ def test_schedule_exchange_counts_at_full_size():
     def count(n, world, ops):
         steps, lay = qc.debug_dist_schedule(n, world, ops)
         assert sorted(lay) == list(range(n))
-        return sum(1 for s in steps if s[0] == 1)
+        # restore exchanges at the end (the layout returns to the relabels-only
+        # one, so a repeated circuit reuses its plan): at most 2 per rank bit
+        p = world.bit_length() - 1
+        assert sum(1 for s in steps if s[0] == 1 and s[3] == 1) <= 2 * p
+        return sum(1 for s in steps if s[0] == 1 and s[3] == 0)
     assert count(36, 8, qcgen.qft(36)) == 4
     assert count(33, 8, qcgen.tfxy(33, 10)) == 51
     assert count(35, 4, qcgen.tfxy(35, 10)) == 31
@@ -175,7 +181,22 @@ def test_pair_segment_schedule():
     # a dense 2-qubit gate on two rank-bit qubits: exchanges bring both local
     u = qcgen.random_unitary(4, np.random.default_rng(0))
     steps, lay = steps_of(14, 4, [qcgen.Op("U2", (0, 1), matrix=u)])
-    assert [s[0] for s in steps].count(1) == 2 and sorted(lay) == list(range(14))
+    assert [s[0] for s in steps if s[3] == 0].count(1) == 2 and sorted(lay) == list(range(14))
+    assert lay == [13 - q for q in range(14)]  # restored
     # gates on local qubits only: one local segment
     steps, _ = steps_of(14, 4, [qcgen.Op("H", (q,)) for q in range(2, 14)])
     assert [s[0] for s in steps] == [0]
+
+
+@pytest.mark.parametrize("n,world", [(16, 4), (18, 8), (36, 8)])
+def test_schedule_restores_relabel_layout(n, world):
+    """Exchange modes 0/1 end every sharded run in the layout the SWAP
+    relabels alone give (so the plan of a repeated circuit is reused)."""
+    for ops in (qcgen.qft(n), qcgen.tfxy(n, 3), qcgen.random_circuit(n, 80, seed=n)):
+        lay = [n - 1 - q for q in range(n)]
+        for op in ops:
+            if op.name == "SWAP":
+                a, b = op.qubits
+                lay[a], lay[b] = lay[b], lay[a]
+        steps, got = qc.debug_dist_schedule(n, world, ops)
+        assert got == lay
