@@ -284,6 +284,16 @@ qc_status qc_state_read(qc_state* s, uint64_t first, uint64_t count, void* host_
  * until the copy has been consumed.  Leaves the layout unchanged. */
 qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void* host_src);
 
+/* Read canonical amplitudes [first, first+count) into host_dst and replace
+ * them with host_src: the same as qc_state_read then qc_state_write, but in
+ * 256 MiB chunks with the upload of chunk c (a second copy stream) overlapping
+ * the read-back of chunk c+1 -- PCIe / C2C links are full duplex, so handing
+ * a result back and loading the next input costs about one direction.  Chunk
+ * c is uploaded only after it has been read, so host_src == host_dst uploads
+ * exactly what was read.  Blocks.  Same range / layout rules as
+ * qc_state_read (a non-canonical single-GPU layout: read, then write). */
+qc_status qc_state_readwrite(qc_state* s, uint64_t first, uint64_t count, void* host_dst, const void* host_src);
+
 /* Permute the amplitudes back to canonical order in place (no-op if already). */
 qc_status qc_state_canonicalize(qc_state* s);
 

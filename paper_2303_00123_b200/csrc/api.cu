@@ -754,6 +754,9 @@ void qc_state_destroy(qc_state* s) {
   if (s->d_stage) cudaFree(s->d_stage);
   if (s->d_partial) cudaFree(s->d_partial);
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->cstream) cudaStreamDestroy(s->cstream);
+  for (cudaEvent_t e : s->cev)
+    if (e) cudaEventDestroy(e);
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
 }
@@ -943,6 +946,58 @@ qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void
   }
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamSynchronize");
+  return QC_OK;
+}
+
+// Read [first, first+count) into host_dst and write host_src in its place,
+// chunk by chunk on two copy streams: the D2H of chunk c+1 (state stream)
+// overlaps the H2D of chunk c (copy stream) -- PCIe is full duplex, so a
+// result read-back and the next input upload take the time of one direction.
+// Chunk c is written only after it has been read, so host_src == host_dst
+// uploads exactly what was read.
+qc_status qc_state_readwrite(qc_state* s, uint64_t first, uint64_t count, void* host_dst, const void* host_src) {
+  qc_status st = check_state(s);
+  if (st != QC_OK) return st;
+  const uint64_t N = 1ull << s->n;
+  if ((!host_dst || !host_src) && count) return fail(QC_ERR_INVALID_ARG, "host buffer is NULL");
+  if (first > N || count > N - first)
+    return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
+                (unsigned long long)count, s->n);
+  if (!count) return QC_OK;
+  if (!layout_is_canonical(s) && s->dist != 2) {  // gather / scatter path: one direction at a time
+    st = qc_state_read(s, first, count, host_dst);
+    return st == QC_OK ? qc_state_write(s, first, count, host_src) : st;
+  }
+  if (s->dist == 2) {
+    const uint64_t nl = 1ull << s->n_loc, lo = (uint64_t)s->rank * nl;
+    if (!layout_is_canonical(s))
+      return fail(QC_ERR_UNSUPPORTED, "sharded state: call qc_state_canonicalize (collective) first");
+    if (first < lo || first + count > lo + nl)
+      return fail(QC_ERR_INVALID_ARG, "sharded state: rank %d holds [%llu, %llu)", s->rank,
+                  (unsigned long long)lo, (unsigned long long)(lo + nl));
+    first -= lo;
+  }
+  cudaError_t e = cudaSuccess;
+  if (!s->cstream) {
+    e = cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&s->cev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(s, e, "copy stream");
+  }
+  const size_t ab = amp_bytes(s);
+  const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / ab);
+  char* dev = (char*)s->d + first * ab;
+  for (uint64_t c = 0; c < count && e == cudaSuccess; c += chunk) {
+    const size_t bytes = std::min<uint64_t>(chunk, count - c) * ab, off = c * ab;
+    e = cudaMemcpyAsync((char*)host_dst + off, dev + off, bytes, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(s->cev[0], s->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s->cstream, s->cev[0], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dev + off, (const char*)host_src + off, bytes, cudaMemcpyHostToDevice, s->cstream);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(s->cev[1], s->cstream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, s->cev[1], 0);  // later work sees the upload
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(s, e, "qc_state_readwrite");
   return QC_OK;
 }
 

@@ -130,6 +130,8 @@ struct qc_state {
   // plan cache
   std::unordered_map<uint64_t, std::unique_ptr<qc::PlanEntry>> plans;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cstream = nullptr;    // qc_state_readwrite: upload stream (D2H stays on `stream`)
+  cudaEvent_t cev[2] = {};
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
   double* d_partial = nullptr;

@@ -52,7 +52,7 @@ EXPORTS = ["qc_state_create", "qc_state_create_ex", "qc_state_wrap", "qc_state_d
            "qc_state_create_dist", "qc_state_create_loopback", "qc_nccl_unique_id",
            "qc_state_init_basis", "qc_state_init_random", "qc_apply_gate", "qc_run_circuit",
            "qc_run_circuit_ex", "qc_apply_mgate",
-           "qc_state_read", "qc_state_write", "qc_state_canonicalize", "qc_state_sync",
+           "qc_state_read", "qc_state_write", "qc_state_readwrite", "qc_state_canonicalize", "qc_state_sync",
            "qc_state_norm2", "qc_set_option", "qc_get_info", "qc_qasm_parse", "qc_qasm_emit",
            "qc_last_error", "qc_version"]
 
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
     L.qc_apply_mgate.argtypes = [vp, vp]
     L.qc_state_read.argtypes = [vp, u64, u64, vp]
     L.qc_state_write.argtypes = [vp, u64, u64, vp]
+    L.qc_state_readwrite.argtypes = [vp, u64, u64, vp, vp]
     L.qc_state_canonicalize.argtypes = [vp]
     L.qc_state_sync.argtypes = [vp]
     L.qc_state_norm2.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
@@ -344,6 +345,10 @@ class State:
 
     def read_ptr(self, host_ptr: int, count: int, first: int = 0):
         _check(lib().qc_state_read(self._h, first, count, host_ptr))
+
+    def readwrite_ptr(self, dst_ptr: int, src_ptr: int, count: int, first: int = 0):
+        """qc_state_readwrite: read [first, +count) into dst, upload src in its place."""
+        _check(lib().qc_state_readwrite(self._h, first, count, dst_ptr, src_ptr))
 
     def exchange(self, g: int, l: int):
         """One qubit-swap exchange of physical rank bit g with local bit l (debug)."""

@@ -243,6 +243,36 @@ def test_read_write_ranges_and_canonicalize(qcmod):
         assert abs(s.norm2() - ref_n2) <= 1e-14 * ref_n2
 
 
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_readwrite_overlapped_copies(qcmod, prec):
+    """qc_state_readwrite == read then write (chunks of 256 MiB: n=25 c128 is
+    2 chunks + a tail of 0; n=26 c64 has 2), distinct and identical host
+    buffers, canonical and relabelled layouts."""
+    dt = np.complex128 if prec == "c128" else np.complex64
+    n = 25 if prec == "c128" else 26
+    with qcmod.State(n, prec) as s:
+        s.init_random(4)
+        before = s.read()
+        src = (np.arange(1 << n) * (1 + 0.5j)).astype(dt)
+        dst = np.zeros(1 << n, dtype=dt)
+        s.readwrite_ptr(dst.ctypes.data, src.ctypes.data, 1 << n)
+        assert np.array_equal(dst, before) and np.array_equal(s.read(), src)
+        # identical buffer: upload what was just read (a round trip), sub-range
+        buf = np.zeros(3000, dtype=dt)
+        s.readwrite_ptr(buf.ctypes.data, buf.ctypes.data, 3000, 777)
+        assert np.array_equal(buf, src[777:3777]) and np.array_equal(s.read(), src)
+    with qcmod.State(12, prec) as s:  # non-canonical layout (QFT relabels)
+        s.init_random(9)
+        s.run(qcgen.qft(12))
+        full = s.read()
+        x = np.full(50, 2 - 1j, dtype=dt)
+        got = np.zeros(50, dtype=dt)
+        s.readwrite_ptr(got.ctypes.data, x.ctypes.data, 50, 1000)
+        full_new = full.copy()
+        full_new[1000:1050] = x
+        assert np.array_equal(got, full[1000:1050]) and np.array_equal(s.read(), full_new)
+
+
 def test_invalid_ops_leave_state_unchanged(qcmod):
     from paper_2303_00123_b200 import QCError
     n = 6
