@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <bit>
+#include <cstdlib>
 #include <cstring>
 
 #include "fused_common.cuh"
@@ -318,6 +319,15 @@ EncodeFn encoder() {
 }
 }  // namespace
 
+// L2 promotion of the box tensor maps (QC_TMAP_PROMO 0 none, 1 64 B, 2 128 B,
+// 3 256 B = default; experiment knob).
+CUtensorMapL2promotion box_promotion() {
+  static const int v = getenv("QC_TMAP_PROMO") ? atoi(getenv("QC_TMAP_PROMO")) : 3;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // 5-D tensor map that moves one whole tile per TMA request (PassDesc g4 == 2).
 // The tile's bit set T (physical bits of an nbits-bit index) splits into runs
 // of consecutive bits; dim d starts at run d and extends up to the next run,
@@ -381,7 +391,7 @@ bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t T, QcTmap* out, Pas
   CUtensorMap tm;
   const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstride, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         box_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   memcpy(out, &tm, sizeof tm);
   return true;
