@@ -744,6 +744,11 @@ def main():
 
     import torch
     if world > 1:
+        # NCCL's init log (ranks, NVLink / NVLS topology) on stderr, so the
+        # communicator size can be checked without touching the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
