@@ -111,3 +111,29 @@ def test_tfxy_parity_sector_full_size(qcmod, n):
             assert np.all(got[par == 1] == 0)
             assert np.any(got[par == 0] != 0)
         assert abs(s.norm2() - 1.0) < 1e-10
+
+
+@pytest.mark.parametrize("n,world,xmode", [(33, 2, 2), (33, 8, 2), (33, 8, 0)])
+def test_sharded_loopback_full_size(qcmod, n, world, xmode):
+    """The sharded path at the C4 size in loopback (all shards in one 137 GB
+    buffer): QFT on a basis state vs the closed form (sampled), through pair
+    passes (mode 2: 64-bit tile offsets of the tile split, two-shard tile
+    halves) or exchanges + the end-of-run layout restore (mode 0)."""
+    if free_bytes() < (16 << n) * 1.1:
+        pytest.skip("not enough device memory")
+    N = 1 << n
+    k = 0x1F2E3D4C % N
+    with qcmod.State.loopback(n, "c128", world) as s:
+        s.set_option("exchange", xmode)
+        arr = qcmod.encode_ops(qcgen.qft(n))
+        for _ in range(2):  # 2nd run: NVRTC-specialised passes
+            s.init_basis(k)
+            s.run(arr)
+        info = s.info()
+        assert info["last_jit"]
+        assert (info["last_pair_segments"] > 0) if xmode == 2 else (info["last_exchanges"] > 0)
+        for j, v in read_samples(s, sample_idx(n, 256, seed=world + xmode)).items():
+            ph = 2.0 * math.pi * ((j * k) % N) / N
+            ref = complex(math.cos(ph), -math.sin(ph)) / math.sqrt(N)
+            assert abs(complex(v) - ref) <= 1e-12, (j, v, ref)
+        assert abs(s.norm2() - 1.0) < 1e-10
