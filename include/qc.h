@@ -104,8 +104,10 @@ typedef enum {
     QC_OPT_TILE_BITS = 3,     /* 0 (default): auto (64 KiB tiles); else 4..13               */
     QC_OPT_CTAS = 4,          /* 0 (default): one CTA per SM; else grid size of fused passes */
     QC_OPT_BLOCK_FUSION = 5,  /* 1 (default): merge gates on <= 2 qubits into exact blocks    */
-    QC_OPT_JIT = 6,           /* 1 (default): specialise repeated fused plans with NVRTC;
-                                 0: never (AOT interpreting kernel); 2: from the first run  */
+    QC_OPT_JIT = 6,           /* 1 (default): specialise repeated fused plans with NVRTC
+                                 (and plans whose passes span >= 2^30 amplitudes from the
+                                 first run); 0: never (AOT interpreting kernel); 2: from
+                                 the first run                                              */
     QC_OPT_ROW_BITS = 7,      /* 0 (default): auto -- with the box transport the planner plans
                                  3..6 (c128) / 4..7 (c64) row bits and keeps the plan a host
                                  cost model prefers; else the contiguous row bits of a tile  */

@@ -510,9 +510,14 @@ int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64
 
 int enqueue_plan(qc_state* s, PlanEntry* e, cudaStream_t st) { return enqueue_entry(s, e, st, s->d, 0, 0); }
 
-// NVRTC-specialise an entry according to the JIT policy (2nd use by default).
+// NVRTC-specialise an entry according to the JIT policy: 2nd use by default,
+// 1st use when a pass spans >= 2^30 amplitudes -- there the interpreting AOT
+// kernel costs more per pass (~25 ms per 2^29 amplitudes over the JIT kernel,
+// measured) than compiling every pass on host threads (~1-3 s once per
+// process; cubins are cached on disk across processes).
 qc_status maybe_jit(qc_state* s, PlanEntry* e) {
-  if (e->jit_state == 0 && e->ir && (s->jit == 2 || (s->jit == 1 && e->uses >= 2))) {
+  const bool big = !e->passes.empty() && (e->passes[0].n_tiles << e->passes[0].k) >= (1ull << 30);
+  if (e->jit_state == 0 && e->ir && (s->jit == 2 || (s->jit == 1 && (e->uses >= 2 || big)))) {
     std::string err;
     if (jit_build(*e->ir, s->dbl, e->jit, err)) {
       e->jit_state = 1;

@@ -137,3 +137,20 @@ def test_sharded_loopback_full_size(qcmod, n, world, xmode):
             ref = complex(math.cos(ph), -math.sin(ph)) / math.sqrt(N)
             assert abs(complex(v) - ref) <= 1e-12, (j, v, ref)
         assert abs(s.norm2() - 1.0) < 1e-10
+
+
+def test_jit_first_use_for_large_states(qcmod):
+    """Passes over >= 2^30 amplitudes are NVRTC-specialised from the first run
+    (the interpreting kernel would cost more than compiling); the result of
+    that first run is the QFT closed form."""
+    n = 30
+    if free_bytes() < (16 << n) * 1.1:
+        pytest.skip("not enough device memory")
+    N, k = 1 << n, 12345
+    with qcmod.State(n, "c128") as s:
+        s.init_basis(k)
+        s.run(qcgen.qft(n))
+        assert s.info()["last_jit"]
+        for j, v in read_samples(s, sample_idx(n, 64, seed=7)).items():
+            ph = 2.0 * math.pi * ((j * k) % N) / N
+            assert abs(complex(v) - complex(math.cos(ph), -math.sin(ph)) / math.sqrt(N)) <= 1e-12
