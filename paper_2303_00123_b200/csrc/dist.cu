@@ -392,13 +392,35 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
       for (PGate& pg : seg)
         if (seg_pair != nl) pgate_swap_bits(pg, nl, seg_pair);
       void* peer = nullptr;
+      const size_t shard_bytes = (size_t)(s->dbl ? 16 : 8) << nl;
       if (s->dist == 2) {
         r = ensure_peers(s);  // collective (same point of the schedule on every rank)
         if (r != QC_OK) return r;
         peer = s->peers[(size_t)(s->rank ^ (1 << (seg_pair - nl)))];
+      } else {
+        peer = (char*)s->d + shard_bytes;  // loopback: shard 1 stands in for "a peer" (maps below)
       }
-      r = build_fused_entry(s, seg, nl + 1, (2ull << nl) - 1, st.seg.get(), s->d, s->dist == 1 ? n : nl,
-                            s->remap != 0, 1ull << nl, peer);
+      // tensor maps over nl bits of one shard (the loopback too: it then
+      // addresses every shard as its own buffer, like the IPC-mapped peers)
+      r = build_fused_entry(s, seg, nl + 1, (2ull << nl) - 1, st.seg.get(), s->d, nl, s->remap != 0, 1ull << nl,
+                            peer);
+      if (r == QC_OK && s->dist == 1) {
+        PlanEntry* e = st.seg.get();
+        e->vr_row.assign((size_t)s->world, QcTmap{});
+        e->vr_box.assign((size_t)s->world, std::vector<QcTmap>(e->passes.size(), QcTmap{}));
+        for (int v = 0; v < s->world && r == QC_OK; ++v) {
+          char* base = (char*)s->d + (size_t)v * shard_bytes;
+          if (!e->passes.empty() && e->passes[0].g4 && !make_row_tmap(base, nl, e->passes[0].rb, s->dbl, &e->vr_row[(size_t)v]))
+            r = fail(QC_ERR_CUDA, "loopback shard row tensor map");
+          for (size_t i = 0; i < e->passes.size() && r == QC_OK; ++i) {
+            PassDesc tmp = e->passes[i];
+            if (e->passes[i].g4 == 2 &&
+                !make_box_tmap(base, nl, s->dbl, pass_tile_set(e->passes[i]) & ~(1ull << nl),
+                               &e->vr_box[(size_t)v][i], &tmp))
+              r = fail(QC_ERR_CUDA, "loopback shard box tensor map");
+          }
+        }
+      }
     }
     if (r != QC_OK) return r;
     P->passes += (int64_t)st.seg->passes.size();
@@ -567,8 +589,11 @@ qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
     void* ptr;
     uint64_t ab;
     bool peer;
+    int vr;  // loopback virtual rank whose shard this is (-1: NCCL rank buffers)
   };
   auto tmap_of = [&](const Buf& b, size_t i) -> const QcTmap& {
+    if (b.vr >= 0)  // loopback: the virtual rank's own shard maps
+      return e->passes[i].g4 == 2 ? e->vr_box[(size_t)b.vr][i] : e->vr_row[(size_t)b.vr];
     if (b.peer) return e->tmaps_peer.empty() ? e->tmap_peer : e->tmaps_peer[i];
     return e->tmaps.empty() ? e->tmap : e->tmaps[i];
   };
@@ -586,10 +611,11 @@ qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
     const uint64_t half = pd.n_tiles / 2;
     pd.n_tiles = half;
     pd.tile0 = v ? half : 0;
-    Buf mine{s->d, 0, false}, peer{nullptr, 0, true};
-    if (s->dist == 1) {  // loopback: shards of one buffer, tensor maps over all n bits
-      mine.ab = (uint64_t)r << nl;
-      peer = Buf{s->d, (uint64_t)partner << nl, false};
+    Buf mine{s->d, 0, false, -1}, peer{nullptr, 0, true, -1};
+    if (s->dist == 1) {  // loopback: every shard addressed as its own buffer (as the P2P peers)
+      const size_t sb = (size_t)(s->dbl ? 16 : 8) << nl;
+      mine = Buf{(char*)s->d + (size_t)r * sb, 0, false, r};
+      peer = Buf{(char*)s->d + (size_t)partner * sb, 0, false, partner};
     } else {
       peer.ptr = s->peers[(size_t)partner];
     }

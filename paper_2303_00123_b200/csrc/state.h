@@ -28,6 +28,11 @@ struct PlanEntry {
   uint64_t pair_mask = 0;            // the pair bit (plan space); 0: not a pair segment
   QcTmap tmap_peer{};                // the partner's buffer (P2P): row tensor map ...
   std::vector<QcTmap> tmaps_peer;    // ... and per-pass box tensor maps
+  // loopback pair segments: tensor maps over each virtual rank's own shard
+  // (nl bits at that shard's base), so the loopback runs the P2P code path
+  // -- separate buffers, addr_bits 0 -- with only the pointers local
+  std::vector<QcTmap> vr_row;               // [rank]
+  std::vector<std::vector<QcTmap>> vr_box;  // [rank][pass]
   bool dbl = true;
   int64_t relabels = 0;
   int uses = 0;
@@ -74,6 +79,7 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
                             uint64_t pair_mask = 0, void* peer_base = nullptr);
 int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
                   uint64_t addr_bits);
+uint64_t pass_tile_set(const PassDesc& d);  // a pass's tile bit set (row bits + hi bits)
 // One pass of an entry with explicit buffers (pair segments: halves in two buffers).
 int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmap& tm,
                 const QcTmap& tm1, cudaStream_t st);
