@@ -136,7 +136,14 @@ typedef enum {
                                    halves from / to both shards directly (TMA over the IPC-
                                    mapped partner buffer): the exchange is fused into the
                                    pass and the layout does not change (no swap back).  A
-                                   gate on two rank-bit qubits at once falls back to 1 */
+                                   gate on two rank-bit qubits at once falls back to 1;
+                                 3: group plan -- the whole circuit planned once over all n
+                                   bits like a single-GPU state; a pass whose tile holds j
+                                   rank bits moves its 2^j sub-tiles from / to 2^j shards
+                                   (one tensor map per shard), the P ranks splitting its
+                                   tiles; passes without rank bits stay in the own shard.
+                                   No exchanges, no layout change; spanning passes are
+                                   bracketed by world barriers                          */
 } qc_option;
 
 /* Counters of the most recent qc_run_circuit / qc_apply_gate. */
@@ -165,7 +172,8 @@ typedef struct qc_info {
                                   the ALU roofline numerator, qc_debug.h)      */
     int64_t last_pair_segments; /* sharded runs with QC_OPT_EXCHANGE 2: pair segments
                                    (gates on one rank-bit qubit run in place over
-                                   the pair's two shards, no exchange)          */
+                                   the pair's two shards, no exchange); with 3:
+                                   passes whose tiles span several shards       */
 } qc_info;
 
 /* Generic gate: any number of controls and a dense

@@ -372,12 +372,12 @@ FusedPlan plan_best(int n_plan, int k, int rb_default, int row_bits_opt, bool bo
 // controls / diagonal bits).  `tmap_base` / `tmap_bits`: the buffer and index
 // width the row tensor map spans.
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
-                            PlanEntry* e, void* tmap_base, int tmap_bits, bool remap, uint64_t pair_mask,
+                            PlanEntry* e, void* tmap_base, int tmap_bits, bool remap, uint64_t group_mask,
                             void* peer_base) {
   int k, rb, ctas;
-  // pair segment: the pair's two ranks split every pass's tiles, so a pass
-  // needs >= 2 tiles (k < n_plan)
-  plan_geometry(s, pair_mask ? n_plan - 1 : n_plan, &k, &rb, &ctas);
+  // plans spanning shards (group_mask = the plan's rank bits): the 2^j ranks
+  // split every pass's tiles, so a pass needs >= 2^j tiles (k <= n_plan - j)
+  plan_geometry(s, n_plan - std::popcount(group_mask), &k, &rb, &ctas);
   e->ctas = ctas;
   e->tile_bits = k;
   std::vector<PGate> blocks = s->block_fusion ? fuse_blocks(gates, local_mask) : gates;
@@ -392,17 +392,17 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   const int tbits = tmap_bits ? tmap_bits : n_plan;
   const bool g4 = (s->tma_mode == 0 || s->tma_mode == 2) && make_row_tmap(tb, tbits, rb, s->dbl, &e->tmap) &&
                   (!peer_base || make_row_tmap(peer_base, tbits, rb, s->dbl, &e->tmap_peer));
-  e->pair_mask = pair_mask;
+  e->pair_mask = group_mask;
   for (auto& p : fp.passes) {
     p.desc.g4 = g4 ? 1 : 0;
     p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding
-    // pair segment: the pair bit never reaches an address (it selects the
-    // buffer); a pass whose tile holds it moves its two halves separately
-    p.desc.addr_strip = pair_mask;
-    p.desc.pair = (pass_tile_set(p.desc) & pair_mask) ? 1 : 0;
+    // rank bits never reach an address (they select the buffer); a pass
+    // whose tile holds j of them moves its 2^j sub-tiles separately
+    p.desc.addr_strip = group_mask;
+    p.desc.grp = std::popcount(pass_tile_set(p.desc) & group_mask);
   }
   if (box) {
-    // one TMA box per tile (per half tile of a pair pass) where the tile's bit
+    // one TMA box per tile (per sub-tile of a tile spanning shards) where the tile's bit
     // runs fit a 5-D tensor map (else that pass keeps the gather4 rows, or
     // per-row copies)
     e->tmaps.assign(fp.passes.size(), e->tmap);
@@ -410,7 +410,7 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
     for (size_t i = 0; i < fp.passes.size(); ++i) {
       PassDesc& d = fp.passes[i].desc;
       PassDesc d2 = d;
-      const uint64_t T = pass_tile_set(d) & ~pair_mask;
+      const uint64_t T = pass_tile_set(d) & ~group_mask;
       if (make_box_tmap(tb, tbits, s->dbl, T, &e->tmaps[i], &d2) &&
           (!peer_base || make_box_tmap(peer_base, tbits, s->dbl, T, &e->tmaps_peer[i], &d2))) {
         d = d2;
@@ -419,8 +419,8 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
       }
     }
   }
-  for (auto& p : fp.passes)  // a gather4 request (4 rows) must not straddle a pair pass's two halves
-    if (p.desc.pair && p.desc.g4 == 1 && p.desc.k - p.desc.rb < 3) {
+  for (auto& p : fp.passes)  // a gather4 request (4 rows) must not straddle two sub-tiles
+    if (p.desc.grp && p.desc.g4 == 1 && p.desc.k - p.desc.rb - p.desc.grp < 2) {
       p.desc.g4 = 0;
       p.desc.pshift = p.desc.rb;
     }
@@ -488,10 +488,10 @@ qc_status get_plan(qc_state* s, const qc_gate* ops, size_t n_ops, const MTable* 
   return QC_OK;
 }
 
-int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmap& tm,
-                const QcTmap& tm1, cudaStream_t st) {
-  return (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, tm, tm1, e->ctas, st)
-                             : launch_fused_pass(base, s->dbl, pd, e->d_blob, tm, tm1, e->ctas, st);
+int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmapSet& tms,
+                cudaStream_t st) {
+  return (e->jit_state == 1) ? jit_launch(e->jit[i], base, pd, tms, e->ctas, st)
+                             : launch_fused_pass(base, s->dbl, pd, e->d_blob, tms, e->ctas, st);
 }
 
 // Launch every pass of a fused entry; rank_bits / addr_bits: see PassDesc.
@@ -501,8 +501,9 @@ int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64
     PassDesc pd = e->passes[i];
     pd.rank_bits = rank_bits;
     pd.addr_bits = addr_bits;
-    const QcTmap& tm = e->tmaps.empty() ? e->tmap : e->tmaps[i];
-    const int r = launch_pass(s, e, i, pd, base, tm, tm, st);
+    QcTmapSet tms;
+    tms.m[0] = e->tmaps.empty() ? e->tmap : e->tmaps[i];
+    const int r = launch_pass(s, e, i, pd, base, tms, st);
     if (r) return r;
   }
   return 0;
@@ -1079,7 +1080,8 @@ qc_status qc_set_option(qc_state* s, qc_option opt, int64_t v) {
       break;
     case QC_OPT_REMAP: s->remap = v != 0; break;
     case QC_OPT_EXCHANGE:
-      if (v < 0 || v > 2) return fail(QC_ERR_INVALID_ARG, "exchange must be 0 (NCCL), 1 (P2P) or 2 (pair passes)");
+      if (v < 0 || v > 3)
+        return fail(QC_ERR_INVALID_ARG, "exchange must be 0 (NCCL), 1 (P2P), 2 (pair passes) or 3 (group plan)");
       s->xmode = (int)v;
       break;
     case QC_OPT_JIT:
@@ -1215,7 +1217,7 @@ extern "C" qc_status qc_debug_dist_schedule(int n, int world, int relabel, const
 extern "C" qc_status qc_debug_dist_schedule_ex(int n, int world, int relabel, int exchange_mode, const qc_gate* ops,
                                               size_t n_ops, int* steps, int max_steps, int* n_steps,
                                               int* layout_out) {
-  if (exchange_mode < 0 || exchange_mode > 2) return fail(QC_ERR_INVALID_ARG, "bad exchange mode");
+  if (exchange_mode < 0 || exchange_mode > 3) return fail(QC_ERR_INVALID_ARG, "bad exchange mode");
   if (!n_steps || world < 2 || (world & (world - 1))) return fail(QC_ERR_INVALID_ARG, "bad arguments");
   for (size_t i = 0; i < n_ops; ++i) {
     const qc_status st = validate_gate(n, ops[i], i);

@@ -44,7 +44,8 @@ struct DistPlan {
   std::vector<uint8_t> mkey;  // referenced generic gates' contents
   std::vector<int> layout_in, layout_out;
   struct Step {
-    int kind = 0;  // 0: fused local segment, 1: exchange, 2: pair segment on rank bit g (QC_OPT_EXCHANGE 2)
+    int kind = 0;  // 0: fused local segment, 1: exchange, 2: pair segment on rank bit g (QC_OPT_EXCHANGE 2),
+                   // 3: the whole circuit as one plan over all n bits (QC_OPT_EXCHANGE 3)
     int g = -1, l = -1;
     bool restore = false;  // exchange that undoes the schedule's permutation at the end
     std::unique_ptr<PlanEntry> seg;
@@ -350,6 +351,61 @@ qc_status build_dist_plan(qc_state* s, const qc_gate* ops, size_t n_ops, DistPla
   std::memcpy(lay, s->layout, sizeof(int) * n);
   std::memcpy(rel, s->layout, sizeof(int) * n);  // the layout after the SWAP relabels only
   for (int q = 0; q < n; ++q) inv[lay[q]] = q;
+  if (s->xmode == 3) {
+    // Group plan: the circuit is planned ONCE over all n bits, exactly like a
+    // single-GPU state; a tile may hold rank bits, its sub-tiles then live in
+    // several shards (PassDesc::grp).  No exchanges; the plan restores its
+    // layout (remap) so only the SWAP relabels change it.
+    std::vector<PGate> gates;
+    for (size_t i = 0; i < n_ops; ++i) {
+      const qc_gate& op = ops[i];
+      if (op.op == QC_SWAP && s->relabel) {
+        std::swap(lay[op.qubits[0]], lay[op.qubits[1]]);
+        P->relabels++;
+        continue;
+      }
+      gates.push_back(lower(op, lay, mt));
+    }
+    DistPlan::Step st;
+    st.kind = 3;
+    st.seg = std::make_unique<PlanEntry>();
+    if (!gates.empty() && !dry_run) {
+      const size_t shard_bytes = (size_t)(s->dbl ? 16 : 8) << nl;
+      if (s->dist == 2) {
+        const qc_status r = ensure_peers(s);  // collective (same point of the schedule on every rank)
+        if (r != QC_OK) return r;
+      }
+      auto buf_of = [&](int q) -> void* {
+        return s->dist == 1 ? (void*)((char*)s->d + (size_t)q * shard_bytes) : s->peers[(size_t)q];
+      };
+      const uint64_t rank_mask = ((n >= 64 ? ~0ull : (1ull << n) - 1)) & ~((1ull << nl) - 1);
+      PlanEntry* e = st.seg.get();
+      qc_status r = build_fused_entry(s, gates, n, ~0ull, e, buf_of(0), nl, s->remap != 0, rank_mask, buf_of(1));
+      // tensor maps over every rank's shard (nl bits at its base)
+      e->vr_row.assign((size_t)s->world, QcTmap{});
+      e->vr_box.assign((size_t)s->world, std::vector<QcTmap>(e->passes.size(), QcTmap{}));
+      for (int v = 0; v < s->world && r == QC_OK; ++v) {
+        if (!e->passes.empty() && e->passes[0].g4 && !make_row_tmap(buf_of(v), nl, e->passes[0].rb, s->dbl, &e->vr_row[(size_t)v]))
+          r = fail(QC_ERR_CUDA, "shard row tensor map");
+        for (size_t i = 0; i < e->passes.size() && r == QC_OK; ++i) {
+          PassDesc tmp = e->passes[i];
+          if (e->passes[i].g4 == 2 &&
+              !make_box_tmap(buf_of(v), nl, s->dbl, pass_tile_set(e->passes[i]) & ~rank_mask, &e->vr_box[(size_t)v][i],
+                             &tmp))
+            r = fail(QC_ERR_CUDA, "shard box tensor map");
+        }
+      }
+      if (r != QC_OK) return r;
+      if (!e->perm.empty())  // remap swaps moved physical bits: the layout follows the data
+        for (int q = 0; q < n; ++q) lay[q] = e->perm[lay[q]];
+      P->passes += (int64_t)e->passes.size();
+      for (const PassDesc& pd : e->passes) P->pair_segments += pd.grp ? 1 : 0;  // passes spanning shards
+    }
+    st.seg->fused_gates = (int64_t)gates.size();
+    if (!gates.empty()) P->steps.push_back(std::move(st));
+    P->layout_out.assign(lay, lay + n);
+    return QC_OK;
+  }
   // next non-diagonal use of each logical qubit after op i (Belady)
   std::vector<std::vector<int>> uses(n);
   for (size_t i = 0; i < n_ops; ++i) {
@@ -619,17 +675,19 @@ qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
     } else {
       peer.ptr = s->peers[(size_t)partner];
     }
-    if (!pd.pair) {
+    QcTmapSet tms;
+    if (!pd.grp) {
       pd.addr_bits = mine.ab;
-      const QcTmap& tm = tmap_of(mine, i);
-      return launch_pass(s, e, i, pd, mine.ptr, tm, tm, s->stream);
+      tms.m[0] = tmap_of(mine, i);
+      return launch_pass(s, e, i, pd, mine.ptr, tms, s->stream);
     }
-    const Buf& h0 = v ? peer : mine;
-    const Buf& h1 = v ? mine : peer;
-    pd.addr_bits = h0.ab;
-    pd.addr_bits1 = h1.ab;
-    pd.state1 = (uint64_t)(uintptr_t)h1.ptr;
-    return launch_pass(s, e, i, pd, h0.ptr, tmap_of(h0, i), tmap_of(h1, i), s->stream);
+    const Buf* hb[2] = {v ? &peer : &mine, v ? &mine : &peer};  // sub-tile h = pair bit h
+    for (int h = 0; h < 2; ++h) {
+      tms.m[h] = tmap_of(*hb[h], i);
+      pd.sub_addr[h] = hb[h]->ab;
+      pd.sub_state[h] = (uint64_t)(uintptr_t)hb[h]->ptr;
+    }
+    return launch_pass(s, e, i, pd, hb[0]->ptr, tms, s->stream);
   };
   const size_t np = e->passes.size();
   if (s->dist == 1) {
@@ -641,7 +699,7 @@ qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
   const int partner = s->rank ^ (1 << j);
   bool prev_pair = false;
   for (size_t i = 0; i < np; ++i) {
-    const bool pr = e->passes[i].pair != 0;
+    const bool pr = e->passes[i].grp != 0;
     if (pr && !prev_pair) {
       const qc_status b = pair_barrier(s, partner);
       if (b != QC_OK) return b;
@@ -656,9 +714,98 @@ qc_status enqueue_pair_segment(qc_state* s, const DistPlan::Step& st) {
   return QC_OK;
 }
 
+// Stream-ordered barrier of all ranks (a 1-byte NCCL all-reduce): every
+// rank's earlier work on its shard is done before anyone's later work.
+qc_status world_barrier(qc_state* s) {
+  const int r = nccl().all_reduce(s->d_token, s->d_token, 1, kNcclUint8, kNcclSum, s->nccl_comm, s->stream);
+  return r ? nccl_fail(s, r, "world barrier") : QC_OK;
+}
+
+// A group plan (kind 3) over all n bits.  Pass i on rank r: the tile's rank
+// bits G (|G| = j) are its top j local bits; the other rank bits O are the
+// top p-j tile-index bits.  Rank r takes the tiles whose O bits equal its own
+// and, of those, the 1/2^j whose next j index bits equal its G bits -- one
+// contiguous range of n_tiles / P tiles.  Sub-tile h of such a tile lives in
+// the rank with r's O bits and G bits = h; a pass with j = 0 stays in the
+// rank's own shard.  Passes with j > 0 are bracketed by world barriers
+// (NCCL); the loopback runs all virtual ranks pass by pass.
+qc_status enqueue_group_plan(qc_state* s, const DistPlan::Step& st) {
+  PlanEntry* e = st.seg.get();
+  const int nl = s->n_loc, p = std::countr_zero((unsigned)s->world);
+  const size_t shard_bytes = (size_t)(s->dbl ? 16 : 8) << nl;
+  auto buf_of = [&](int q) -> void* {
+    return s->dist == 1 ? (void*)((char*)s->d + (size_t)q * shard_bytes) : s->peers[(size_t)q];
+  };
+  auto map_of = [&](int q, size_t i) -> const QcTmap& {
+    return e->passes[i].g4 == 2 ? e->vr_box[(size_t)q][i] : e->vr_row[(size_t)q];
+  };
+  auto pext = [](uint32_t x, uint32_t m) {
+    uint32_t r = 0;
+    for (int b = 0, o = 0; b < 32; ++b)
+      if ((m >> b) & 1u) r |= ((x >> b) & 1u) << o++;
+    return r;
+  };
+  auto pdep = [](uint32_t x, uint32_t m) {
+    uint32_t r = 0;
+    for (int b = 0, o = 0; b < 32; ++b)
+      if ((m >> b) & 1u) r |= ((x >> o++) & 1u) << b;
+    return r;
+  };
+  const uint32_t all = (1u << p) - 1u;
+  auto launch_rank = [&](int r, size_t i) -> int {
+    PassDesc pd = e->passes[i];
+    const uint32_t G = (uint32_t)(pass_tile_set(pd) >> nl) & all;
+    const int j = std::popcount(G);
+    const int tb = std::countr_zero(pd.n_tiles);
+    pd.n_tiles >>= p;
+    pd.tile0 = ((uint64_t)pext((uint32_t)r, all & ~G) << (tb - (p - j))) | ((uint64_t)pext((uint32_t)r, G) << (tb - p));
+    pd.rank_bits = 0;
+    pd.addr_bits = 0;
+    QcTmapSet tms;
+    if (!j) {
+      tms.m[0] = map_of(r, i);
+      return launch_pass(s, e, i, pd, buf_of(r), tms, s->stream);
+    }
+    for (uint32_t h = 0; h < (1u << j); ++h) {
+      const int q = (int)(((uint32_t)r & ~G) | pdep(h, G));
+      tms.m[h] = map_of(q, i);
+      pd.sub_addr[h] = 0;
+      pd.sub_state[h] = (uint64_t)(uintptr_t)buf_of(q);
+    }
+    return launch_pass(s, e, i, pd, buf_of((int)((uint32_t)r & ~G)), tms, s->stream);
+  };
+  const size_t np = e->passes.size();
+  if (s->dist == 1) {
+    for (size_t i = 0; i < np; ++i)
+      for (int r = 0; r < s->world; ++r)
+        if (const int rc = launch_rank(r, i)) return cuda_fail(s, rc, "group plan pass (loopback)");
+    return QC_OK;
+  }
+  bool prev = false;
+  for (size_t i = 0; i < np; ++i) {
+    const bool spans = e->passes[i].grp != 0;
+    if (spans && !prev) {
+      const qc_status b = world_barrier(s);
+      if (b != QC_OK) return b;
+    }
+    if (const int rc = launch_rank(s->rank, i)) return cuda_fail(s, rc, "group plan pass");
+    if (spans) {
+      const qc_status b = world_barrier(s);
+      if (b != QC_OK) return b;
+    }
+    prev = spans;
+  }
+  return QC_OK;
+}
+
 qc_status enqueue_dist(qc_state* s, DistPlan* P) {
   const uint64_t nloc_amps = 1ull << s->n_loc;
   for (auto& st : P->steps) {
+    if (st.kind == 3) {
+      const qc_status r = enqueue_group_plan(s, st);
+      if (r != QC_OK) return r;
+      continue;
+    }
     if (st.kind == 2) {
       const qc_status r = enqueue_pair_segment(s, st);
       if (r != QC_OK) return r;

@@ -398,14 +398,14 @@ __device__ __forceinline__ void qc_prun_slot(C (&v)[kSlots], const C w0, const C
 //   void setup(unsigned char* extra, const PassDesc&)   all threads, before sync
 //   void prologue(uint64_t tbase, int par)             compute threads, per tile
 //   void tile(C* buf, uint64_t tbase, int par)          compute threads, per tile
-// Tile transport of a pair pass (pd.pair): the top tile-local bit is the
-// pair bit, so the tile's lower half (pair bit 0) and upper half (pair bit 1)
-// are moved separately, each from / to its own buffer (tmap / tmap1, state /
-// state1, addr_bits / addr_bits1); every other pass has one half.
+// Tile transport of a tile spanning shards (pd.grp = j > 0): its top j
+// tile-local bits are rank bits, so its 2^j sub-tiles (2^(k-j) amplitudes
+// each, contiguous in smem) are moved separately, each from / to its own
+// buffer (tmaps->m[h], sub_state[h], sub_addr[h]); other passes: one sub-tile
+// (tmaps->m[0], state, addr_bits).
 template <typename C, int NBUF, class Body>
 __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const PassDesc& pd,
-                                                  const QcTmap* tmap, const QcTmap* tmap1, unsigned char* smem_raw,
-                                                  Body& body) {
+                                                  const QcTmapSet* tmaps, unsigned char* smem_raw, Body& body) {
   const int rb = pd.rb, k = pd.k, ps = pd.pshift;
   const uint32_t PAD = kPadBytes / sizeof(C);
   const uint32_t row_amps = 1u << rb;
@@ -461,15 +461,15 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
         const uint64_t base = qc_tile_base(pd, pd.tile0 + blockIdx.x + ip * gridDim.x) & ~pd.addr_strip;
         if (pd.g4 == 2) {
           if (lane == 0) {
-            for (int h = 0; h <= pd.pair; ++h) {
+            for (int h = 0; h < (1 << pd.grp); ++h) {
               int32_t c[5];
-              qc_box_coords<C>(pd, base | (h ? pd.addr_bits1 : pd.addr_bits), c);
+              qc_box_coords<C>(pd, base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits), c);
               const int32_t c4 = c[4];
-              C* hb = buf + ((size_t)h << (k - 1));
+              C* hb = buf + ((size_t)h << (k - pd.grp));
               uint32_t v = 0, j = 0;
               do {  // every combination of the extra tile bits (one box if none)
                 c[4] = c4 | (int32_t)v;
-                qc_box_store(h ? tmap1 : tmap, c, hb + ((size_t)j << pd.bx_sub));
+                qc_box_store(&tmaps->m[h], c, hb + ((size_t)j << pd.bx_sub));
                 v = (v - pd.bx_xmask) & pd.bx_xmask;
                 ++j;
               } while (v);
@@ -477,17 +477,18 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
           }
         } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128) {
-            const bool h = pd.pair && r >= nrows / 2;
-            const uint64_t bb = base | (h ? pd.addr_bits1 : pd.addr_bits);
-            qc_scatter4(h ? tmap1 : tmap, (int32_t)((bb | row_off[r]) >> rb), (int32_t)((bb | row_off[r + 1]) >> rb),
+            const int h = (int)(r >> (k - rb - pd.grp));  // sub-tile: the row's top grp bits
+            const uint64_t bb = base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits);
+            qc_scatter4(&tmaps->m[h], (int32_t)((bb | row_off[r]) >> rb), (int32_t)((bb | row_off[r + 1]) >> rb),
                         (int32_t)((bb | row_off[r + 2]) >> rb), (int32_t)((bb | row_off[r + 3]) >> rb),
                         buf + row_at(r));
           }
         } else {
           for (uint32_t r = lane; r < nrows; r += 32) {
-            const bool h = pd.pair && r >= nrows / 2;
-            C* st = h ? reinterpret_cast<C*>(pd.state1) : state;
-            qc_bulk_s2g(st + (base | (h ? pd.addr_bits1 : pd.addr_bits) | row_off[r]), buf + row_at(r), row_bytes);
+            const int h = (int)(r >> (k - rb - pd.grp));
+            C* st = pd.grp ? reinterpret_cast<C*>(pd.sub_state[h]) : state;
+            qc_bulk_s2g(st + (base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits) | row_off[r]), buf + row_at(r),
+                        row_bytes);
           }
         }
         qc_bulk_commit();
@@ -505,15 +506,15 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
         __syncwarp();
         if (pd.g4 == 2) {
           if (lane == 0) {
-            for (int h = 0; h <= pd.pair; ++h) {
+            for (int h = 0; h < (1 << pd.grp); ++h) {
               int32_t c[5];
-              qc_box_coords<C>(pd, base | (h ? pd.addr_bits1 : pd.addr_bits), c);
+              qc_box_coords<C>(pd, base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits), c);
               const int32_t c4 = c[4];
-              C* hb = buf + ((size_t)h << (k - 1));
+              C* hb = buf + ((size_t)h << (k - pd.grp));
               uint32_t v = 0, j = 0;
               do {
                 c[4] = c4 | (int32_t)v;
-                qc_box_load(hb + ((size_t)j << pd.bx_sub), h ? tmap1 : tmap, c, &full[b]);
+                qc_box_load(hb + ((size_t)j << pd.bx_sub), &tmaps->m[h], c, &full[b]);
                 v = (v - pd.bx_xmask) & pd.bx_xmask;
                 ++j;
               } while (v);
@@ -521,18 +522,18 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
           }
         } else if (pd.g4) {
           for (uint32_t r = 4 * lane; r < nrows; r += 128) {
-            const bool h = pd.pair && r >= nrows / 2;
-            const uint64_t bb = base | (h ? pd.addr_bits1 : pd.addr_bits);
-            qc_gather4(buf + row_at(r), h ? tmap1 : tmap, (int32_t)((bb | row_off[r]) >> rb),
+            const int h = (int)(r >> (k - rb - pd.grp));
+            const uint64_t bb = base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits);
+            qc_gather4(buf + row_at(r), &tmaps->m[h], (int32_t)((bb | row_off[r]) >> rb),
                        (int32_t)((bb | row_off[r + 1]) >> rb), (int32_t)((bb | row_off[r + 2]) >> rb),
                        (int32_t)((bb | row_off[r + 3]) >> rb), &full[b]);
           }
         } else {
           for (uint32_t r = lane; r < nrows; r += 32) {
-            const bool h = pd.pair && r >= nrows / 2;
-            const C* st = h ? reinterpret_cast<const C*>(pd.state1) : state;
-            qc_bulk_g2s(buf + row_at(r), st + (base | (h ? pd.addr_bits1 : pd.addr_bits) | row_off[r]), row_bytes,
-                        &full[b]);
+            const int h = (int)(r >> (k - rb - pd.grp));
+            const C* st = pd.grp ? reinterpret_cast<const C*>(pd.sub_state[h]) : state;
+            qc_bulk_g2s(buf + row_at(r), st + (base | (pd.grp ? pd.sub_addr[h] : pd.addr_bits) | row_off[r]),
+                        row_bytes, &full[b]);
           }
         }
       }

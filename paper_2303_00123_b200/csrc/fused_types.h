@@ -74,6 +74,11 @@ struct SubStageDesc {
 struct alignas(64) QcTmap {
   uint64_t opaque[16];
 };
+// The tensor maps of one launch: m[0] for a tile in one buffer, m[h] for
+// sub-tile h of a tile spanning shards (PassDesc::grp).
+struct alignas(64) QcTmapSet {
+  QcTmap m[8];
+};
 
 struct PassDesc {
   int32_t k, rb;          // tile bits, row bits (T contains physical 0..rb-1)
@@ -98,18 +103,16 @@ struct PassDesc {
   uint64_t rank_bits;     // sharded state: this rank's global bits (rank << n_loc), OR-ed
                           // into every tile's base for predicates / diagonal bits only
   uint64_t addr_bits;     // OR-ed into amplitude addresses (loopback: shards share one buffer)
-  // Pair segments of a sharded state (QC_OPT_EXCHANGE 2, dist.cu): the plan
-  // spans the n_loc local bits plus ONE rank bit, placed at plan bit n_loc
-  // (the "pair bit"); the two ranks that differ in it split every pass's
-  // tiles in half.
+  // Tiles spanning shards (dist.cu: pair segments, QC_OPT_EXCHANGE 2, and
+  // group plans, 3): the plan's index includes rank bits; a tile may hold j
+  // of them (`grp`), always its top j local bits, and then its 2^j sub-tiles
+  // (indexed by those bits' value h) live in 2^j ranks' buffers.
   uint64_t tile0;         // first tile index of this launch (n_tiles = tiles of this launch)
   uint64_t addr_strip;    // plan bits cleared from tile bases / row offsets before addressing
-  uint64_t addr_bits1;    // pair == 1: addr_bits of the pair-bit-1 half of every tile
-  uint64_t state1;        // pair == 1: buffer holding the pair-bit-1 half (per-row copy transport)
-  int32_t pair;           // 1: the tile's top local bit is the pair bit -- its two halves live
-                          // in two buffers (tmap / state / addr_bits and tmap1 / state1 /
-                          // addr_bits1: the ranks' own shard and its partner's, over NVLink)
+  int32_t grp;            // j (<= 3): sub-tile h moves via tmaps.m[h], sub_state[h], sub_addr[h]
   int32_t pad1_;
+  uint64_t sub_addr[8];   // grp > 0: addr_bits of sub-tile h (OR-ed into its addresses)
+  uint64_t sub_state[8];  // grp > 0: buffer of sub-tile h (per-row copy transport)
 };
 
 }  // namespace qc

@@ -229,12 +229,11 @@ struct InterpBody {
 template <typename T, int NBUF>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     fused_pass_kernel(typename CT<T>::type* __restrict__ state, const PassDesc pd,
-                      const uint8_t* __restrict__ gblob, const __grid_constant__ QcTmap tmap,
-                      const __grid_constant__ QcTmap tmap1) {
+                      const uint8_t* __restrict__ gblob, const __grid_constant__ QcTmapSet tmaps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   InterpBody<T> body;
   body.gblob = gblob;
-  qc_fused_pipeline<typename CT<T>::type, NBUF>(state, pd, &tmap, &tmap1, smem_raw, body);
+  qc_fused_pipeline<typename CT<T>::type, NBUF>(state, pd, &tmaps, smem_raw, body);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
@@ -270,7 +269,7 @@ int configure_t() {
 }
 
 template <typename T>
-int launch_t(void* state, const PassDesc& pd, const void* d_blob, const QcTmap& tm, const QcTmap& tm1, int ctas,
+int launch_t(void* state, const PassDesc& pd, const void* d_blob, const QcTmapSet& tms, int ctas,
              cudaStream_t st) {
   using C = typename CT<T>::type;
   const int nb = pick_nbuf<T>(pd);
@@ -281,10 +280,10 @@ int launch_t(void* state, const PassDesc& pd, const void* d_blob, const QcTmap& 
   C* s = reinterpret_cast<C*>(state);
   auto blob = reinterpret_cast<const uint8_t*>(d_blob);
   switch (nb) {
-    case 4: fused_pass_kernel<T, 4><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm, tm1); break;
-    case 3: fused_pass_kernel<T, 3><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm, tm1); break;
-    case 2: fused_pass_kernel<T, 2><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm, tm1); break;
-    default: fused_pass_kernel<T, 1><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tm, tm1); break;
+    case 4: fused_pass_kernel<T, 4><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tms); break;
+    case 3: fused_pass_kernel<T, 3><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tms); break;
+    case 2: fused_pass_kernel<T, 2><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tms); break;
+    default: fused_pass_kernel<T, 1><<<(unsigned)grid, kFusedThreads, smem, st>>>(s, pd, blob, tms); break;
   }
   return (int)cudaGetLastError();
 }
@@ -293,11 +292,11 @@ int launch_t(void* state, const PassDesc& pd, const void* d_blob, const QcTmap& 
 
 int fused_configure(bool dbl) { return dbl ? configure_t<double>() : configure_t<float>(); }
 
-int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_blob, const QcTmap& tm,
-                      const QcTmap& tm1, int ctas, void* stream) {
+int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_blob, const QcTmapSet& tms,
+                      int ctas, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return dbl ? launch_t<double>(state, pd, d_blob, tm, tm1, ctas, st)
-             : launch_t<float>(state, pd, d_blob, tm, tm1, ctas, st);
+  return dbl ? launch_t<double>(state, pd, d_blob, tms, ctas, st)
+             : launch_t<float>(state, pd, d_blob, tms, ctas, st);
 }
 
 namespace {

@@ -582,10 +582,9 @@ void emit_pass(int n, int k, int rb, uint64_t T, const std::vector<Group>& group
   d.addr_bits = 0;
   d.tile0 = 0;
   d.addr_strip = 0;
-  d.addr_bits1 = 0;
-  d.state1 = 0;
-  d.pair = 0;
+  d.grp = 0;
   d.pad1_ = 0;
+  for (int h = 0; h < 8; ++h) d.sub_addr[h] = d.sub_state[h] = 0;
   d.n_hi = 0;
   for (int p = rb; p < n; ++p)
     if (T & (1ull << p)) d.hi_pos[d.n_hi++] = p;

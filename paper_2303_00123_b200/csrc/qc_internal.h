@@ -145,15 +145,15 @@ struct JitKernel {
 };
 bool jit_available(std::string* why);
 bool jit_build(const FusedPlan& plan, bool dbl, std::vector<JitKernel>& out, std::string& err);
-int jit_launch(const JitKernel& k, void* state, const PassDesc& pd, const QcTmap& tm, const QcTmap& tm1,
-               int ctas, void* stream);
+int jit_launch(const JitKernel& k, void* state, const PassDesc& pd, const QcTmapSet& tms, int ctas,
+               void* stream);
 bool jit_compile_only(const FusedPlan& plan, bool dbl, int& compiled, std::string& err);
 std::string jit_source_for_test(const FusedPlan& plan, bool dbl, size_t pass);
 
 // Launchers (kernels_*.cu).  All enqueue on `stream`; return cudaError_t as int.
 int launch_gate(void* state, int n, bool dbl, const PGate& g, void* stream);
-int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_blob, const QcTmap& tm,
-                      const QcTmap& tm1, int ctas, void* stream);
+int launch_fused_pass(void* state, bool dbl, const PassDesc& pd, const void* d_blob, const QcTmapSet& tms,
+                      int ctas, void* stream);
 bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out);
 bool make_box_tmap(void* base, int nbits, bool dbl, uint64_t tile_bits_set, QcTmap* out, PassDesc* d);
 int fused_configure(bool dbl);

@@ -76,13 +76,13 @@ qc_status validate_gate(int n, const qc_gate& g, size_t idx, const MTable* mt = 
 uint64_t hash_ops(const qc_gate* ops, size_t n, const int* layout, int nq, uint64_t salt);
 qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_plan, uint64_t local_mask,
                             PlanEntry* e, void* tmap_base = nullptr, int tmap_bits = 0, bool remap = false,
-                            uint64_t pair_mask = 0, void* peer_base = nullptr);
+                            uint64_t group_mask = 0, void* peer_base = nullptr);
 int enqueue_entry(qc_state* s, PlanEntry* e, cudaStream_t st, void* base, uint64_t rank_bits,
                   uint64_t addr_bits);
 uint64_t pass_tile_set(const PassDesc& d);  // a pass's tile bit set (row bits + hi bits)
 // One pass of an entry with explicit buffers (pair segments: halves in two buffers).
-int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmap& tm,
-                const QcTmap& tm1, cudaStream_t st);
+int launch_pass(qc_state* s, PlanEntry* e, size_t i, const PassDesc& pd, void* base, const QcTmapSet& tms,
+                cudaStream_t st);
 qc_status maybe_jit(qc_state* s, PlanEntry* e);
 qc_status ensure_fused_configured(qc_state* s);
 extern const int kArity[16];

@@ -1,8 +1,9 @@
 """Loopback sharded circuit time, exchange modes side by side (one GPU):
-QC_OPT_EXCHANGE 0 (qubit-swap exchanges as in-place swap kernels) vs 2 (pair
-passes: tile halves from two shards).  On one GPU both halves are local HBM,
-so this checks the pair transport costs no more than a local pass; NVLink
-rates need >= 2 GPUs.
+QC_OPT_EXCHANGE 0 (qubit-swap exchanges as in-place swap kernels), 2 (pair
+passes: tile halves from two shards) and 3 (group plan: one plan over all n
+bits, tiles spanning up to all shards).  On one GPU every shard is local HBM,
+so this checks the multi-buffer tile transport costs no more than a local
+pass, and counts passes; NVLink rates need >= 2 GPUs.
 
   python scripts/time_pair.py qft:30:2 tfxy:28:2 ...   (family:n:world)
 """
@@ -17,7 +18,7 @@ for w in sys.argv[1:]:
     n, world = int(n), int(world)
     ops = qcgen.qft(n) if fam == "qft" else qcgen.tfxy(n, 10)
     arr = qc.encode_ops(ops)
-    for xm in (0, 2):
+    for xm in (0, 2, 3):
         with qc.State.loopback(n, "c128", world) as s:
             s.set_option("exchange", xm)
             s.init_random(1)

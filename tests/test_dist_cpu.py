@@ -200,3 +200,19 @@ def test_schedule_restores_relabel_layout(n, world):
                 lay[a], lay[b] = lay[b], lay[a]
         steps, got = qc.debug_dist_schedule(n, world, ops)
         assert got == lay
+
+
+def test_group_plan_schedule():
+    """QC_OPT_EXCHANGE 3: the whole circuit is one step (a plan over all n
+    bits), no exchanges; the layout changes by the SWAP relabels only."""
+    for n, world, ops in ((36, 8, qcgen.qft(36)), (34, 2, qcgen.tfxy(34, 10)),
+                          (16, 4, qcgen.random_circuit(16, 60, seed=5))):
+        steps, lay = qc.debug_dist_schedule(n, world, ops, exchange=3)
+        assert [s[0] for s in steps] == [3]
+        assert steps[0][3] == sum(1 for op in ops if op.name != "SWAP")
+        want = [n - 1 - q for q in range(n)]
+        for op in ops:
+            if op.name == "SWAP":
+                a, b = op.qubits
+                want[a], want[b] = want[b], want[a]
+        assert lay == want

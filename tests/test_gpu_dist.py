@@ -148,3 +148,43 @@ def test_pair_passes_permutation_bit_exact(qcmod):
     got, info = run_lb(qcmod, n, "c128", world, ops, exchange=2)
     assert info["last_pair_segments"] > 0
     assert np.array_equal(got, ref(n, "c128", ops))
+
+
+# ---- group plans (QC_OPT_EXCHANGE 3): the whole circuit planned once over
+# all n bits; a pass whose tile holds j rank bits moves its 2^j sub-tiles
+# from / to 2^j shards (every shard its own buffer + tensor maps, as the
+# IPC-mapped peers of the NCCL path); no exchanges, no layout drift.
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("world,n", [(2, 13), (4, 14), (8, 16)])
+def test_group_plan_random_circuits(qcmod, prec, world, n):
+    ops = qcgen.random_circuit(n, 150, seed=90 + n + world)
+    got, info = run_lb(qcmod, n, prec, world, ops, exchange=3)
+    assert info["last_exchanges"] == 0 and info["last_pair_segments"] > 0  # passes spanning shards
+    assert maxerr(got, ref(n, prec, ops)) <= TOL[prec]
+
+
+@pytest.mark.parametrize("world,n", [(2, 14), (4, 16), (8, 18)])
+def test_group_plan_qft_tfxy(qcmod, world, n):
+    for ops in (qcgen.qft(n), qcgen.tfxy(n, 3)):
+        # 3 runs: QFT's relabels alternate two layouts (two plans), the 3rd
+        # run is a plan's 2nd use -- NVRTC-specialised
+        got, info = run_lb(qcmod, n, "c128", world, ops, reps=3, exchange=3)
+        assert info["last_exchanges"] == 0 and info["last_jit"]
+        assert maxerr(got, ref(n, "c128", ops, reps=3)) <= 1e-12
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(tma_mode=2), dict(tma_mode=1), dict(remap=0), dict(jit=0),
+                                  dict(relabel_swap=0)])
+def test_group_plan_transports(qcmod, opts):
+    n, world = 15, 8
+    ops = qcgen.qft(n) + qcgen.random_circuit(n, 80, seed=13) + qcgen.random_mcu_circuit(n, 10, seed=3)
+    got, info = run_lb(qcmod, n, "c128", world, ops, reps=2, exchange=3, **opts)
+    assert info["last_pair_segments"] > 0
+    assert maxerr(got, ref(n, "c128", ops, reps=2)) <= 1e-12
+
+
+def test_group_plan_permutation_bit_exact(qcmod):
+    n, world = 14, 4
+    ops = qcgen.random_circuit(n, 200, seed=29, kinds=("X", "CNOT", "SWAP", "CCX"))
+    got, info = run_lb(qcmod, n, "c128", world, ops, exchange=3)
+    assert np.array_equal(got, ref(n, "c128", ops))

@@ -2,7 +2,8 @@
 every rank's canonical shard after QFT / TFXY / random (incl. generic) circuits
 vs the CPU oracle, for every exchange backend (QC_OPT_EXCHANGE 0: NCCL
 send/recv with ping-pong staging, 1: P2P swap kernel over CUDA IPC, 2: pair
-passes reading / writing the partner's shard over the IPC mapping), and
+passes reading / writing the partner's shard over the IPC mapping, 3: one
+group plan whose tiles may span every shard), and
 qc_state_init_basis on a shard.  Skipped on boxes with one GPU (the loopback
 backend in test_gpu_dist.py covers the same schedule on one GPU)."""
 import numpy as np
@@ -73,7 +74,7 @@ def _run(world, n, prec, kind, xmode):
 
 
 @need2
-@pytest.mark.parametrize("xmode", [0, 1, 2])
+@pytest.mark.parametrize("xmode", [0, 1, 2, 3])
 @pytest.mark.parametrize("kind,prec", [("qft", "c128"), ("tfxy", "c128"), ("random", "c128"), ("qft", "c64")])
 def test_nccl_shards_match_oracle(kind, prec, xmode):
     world = 2
