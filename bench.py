@@ -272,6 +272,39 @@ def make_state(args, n, prec, rank, world, local_rank):
     return qc.State.dist(n, prec, rank, world, uid[0])
 
 
+def choose_exchange_mode(rank, world):
+    """Sharded runs: group plans (QC_OPT_EXCHANGE 3: one plan over all n bits,
+    tiles spanning shards through TMA on IPC-mapped peer buffers) if a probe
+    job -- its own processes, launched before any shard is allocated, so a
+    fault cannot take this run down -- reproduces the NCCL-exchange results on
+    this node; else qubit-swap exchanges over NCCL (mode 0).
+    QC_BENCH_EXCHANGE=<mode> skips the probe."""
+    import torch
+    forced = os.environ.get("QC_BENCH_EXCHANGE")
+    if forced is not None:
+        return int(forced), {"mode": int(forced), "probe": "skipped (QC_BENCH_EXCHANGE)"}
+    res = [None]
+    if rank == 0:
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK",
+                            "MASTER_ADDR", "MASTER_PORT") and not k.startswith("TORCHELASTIC")}
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(ROOT, "scripts", "probe_sharded.py")]
+        t0 = time.time()
+        try:
+            r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=420)
+            ok = r.returncode == 0 and "PROBE OK" in r.stdout
+            why = "PROBE OK" if ok else f"rc={r.returncode}: {(r.stdout + r.stderr).strip().splitlines()[-1:]}"
+        except Exception as e:  # timeout / launch failure: stay on the NCCL exchanges
+            ok, why = False, repr(e)[:200]
+        res = [{"ok": ok, "why": why, "seconds": round(time.time() - t0, 1)}]
+    torch.distributed.broadcast_object_list(res, src=0)
+    r = res[0]
+    mode = 3 if r["ok"] else 0
+    return mode, {"mode": mode, "probe": r}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -285,7 +318,10 @@ def run_ours(args, rank, world, local_rank):
     ops = build_ops(args.config, n)
     import paper_2303_00123_b200 as qc
     arr = qc.encode_ops(ops)
+    xmode, xinfo = choose_exchange_mode(rank, world) if world > 1 else (0, None)
     s = make_state(args, n, prec, rank, world, local_rank)
+    if world > 1:
+        s.set_option("exchange", xmode)
     stream = torch.cuda.ExternalStream(s.stream, device=dev)
     s.init_random(12345)
     ab = 16 if prec == "c128" else 8
@@ -330,8 +366,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         ex = {}
         bytes_dir = shard_bytes // 2
-        for xmode, name in ((0, "nccl_sendrecv_pingpong"), (1, "p2p_swap_kernel")):
-            s.set_option("exchange", xmode)
+        for xm_t, name in ((0, "nccl_sendrecv_pingpong"), (1, "p2p_swap_kernel")):
+            s.set_option("exchange", xm_t)
             torch.distributed.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
@@ -346,30 +382,33 @@ def run_ours(args, rank, world, local_rank):
                         "GBps_per_direction": bytes_dir / (te / 1e3) / 1e9,
                         "frac_of_900": bytes_dir / (te / 1e3) / 1e9 / 900.0}
         s.set_option("exchange", 0)
-    if world > 1 and os.environ.get("QC_BENCH_PAIR", "0") == "1":
-        # the same circuit with collective-fused pair passes (QC_OPT_EXCHANGE 2:
-        # gates on one rank-bit qubit run in place over both shards, no
-        # exchange), timed like the headline; the headline keeps mode 0.
-        # Opt-in: TMA over IPC-mapped peer memory has never run on hardware
-        # here (1-GPU boxes), and a fault would cost the whole bench line.
-        s.set_option("exchange", 2)
-        with torch.cuda.stream(stream):
-            s.run(arr)
-            torch.cuda.synchronize()
-            torch.distributed.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(max(1, min(args.steps, 3))):
+    if world > 1:
+        # the same circuit in the other sharded modes (exchanges over NCCL;
+        # pair passes and group plans only if the probe cleared peer-memory
+        # TMA), timed like the headline over a few steps
+        ex["headline_exchange_mode"] = xinfo
+        alts = [m for m in (0, 2, 3) if m != xmode and (m == 0 or xmode == 3)]
+        for m in alts:
+            s.set_option("exchange", m)
+            with torch.cuda.stream(stream):
                 s.run(arr)
-            e1.record(stream)
-            torch.cuda.synchronize()
-        tp = _max_over_ranks(e0.elapsed_time(e1) / max(1, min(args.steps, 3)), world, dev)
-        pi = s.info()
-        ex["pair_passes_circuit"] = {"ms_per_step": tp, "value": gamp(ops, n, tp / 1e3), "unit": UNIT,
-                                     "pair_segments": pi["last_pair_segments"], "passes": pi["last_passes"],
-                                     "exchanges": pi["last_exchanges"]}
-        s.set_option("exchange", 0)
-        s.run(arr)  # back to the mode-0 plan (warm) before e2e
+                s.run(arr)
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k_alt = max(1, min(args.steps, 3))
+                e0.record(stream)
+                for _ in range(k_alt):
+                    s.run(arr)
+                e1.record(stream)
+                torch.cuda.synchronize()
+            tp = _max_over_ranks(e0.elapsed_time(e1) / k_alt, world, dev)
+            pi = s.info()
+            ex[f"circuit_exchange_mode_{m}"] = {
+                "ms_per_step": tp, "value": gamp(ops, n, tp / 1e3), "unit": UNIT, "passes": pi["last_passes"],
+                "exchanges": pi["last_exchanges"], "pair_segments_or_spanning_passes": pi["last_pair_segments"]}
+        s.set_option("exchange", xmode)
+        s.run(arr)  # back to the headline mode's plan (warm) before e2e
 
     # ---- e2e: pinned host state in, circuit, full state out, every step
     # (states above 8 GiB share one pinned buffer for input and output: the
@@ -474,7 +513,9 @@ def run_ours(args, rank, world, local_rank):
                    "initial_state": "splitmix64 seed 12345 (DESIGN input recipe)",
                    "l2": ("flushed (512 MiB write) between timed iterations" if small else
                           f"inputs larger than L2: {shard_bytes / 1e9:.1f} GB per GPU >> 126 MB"),
-                   "parallelism": "single GPU" if world == 1 else f"sharded x{world} by the top {p} qubits (NCCL)",
+                   "parallelism": "single GPU" if world == 1 else
+                   f"sharded x{world} by the top {p} qubits, exchange mode {xmode} "
+                   f"({'group plan: tiles spanning shards over NVLink' if xmode == 3 else 'NCCL qubit-swap exchanges'})",
                    "fused_passes_per_step": passes, "exchanges_per_step": info.get("last_exchanges", 0),
                    "tile_bits": info["tile_bits"], "cuda_graph": info["last_graph"],
                    "jit_specialised": info["last_jit"], "ops_after_block_fusion": info["last_blocks"],
