@@ -445,7 +445,8 @@ int score_tile(const std::vector<PGate>& gates, const std::vector<int>& rem, uin
 
 // Tile set for the next pass: in-order greedy growth from `fixed`, then hill
 // climbing over single-bit exchanges (bits of `fixed` stay) on score_tile.
-uint64_t choose_tile(const std::vector<PGate>& gates, const std::vector<int>& rem, uint64_t fixed, int k, int n) {
+uint64_t choose_tile(const std::vector<PGate>& gates, const std::vector<int>& rem, uint64_t fixed, int k, int n,
+                     int seeds) {
   uint64_t T = fixed, blocked = 0;
   for (int gi : rem) {
     const PGate& g = gates[gi];
@@ -459,28 +460,67 @@ uint64_t choose_tile(const std::vector<PGate>& gates, const std::vector<int>& re
     else blocked |= all;
   }
   const uint64_t full = n >= 64 ? ~0ull : (1ull << n) - 1;
-  int best = score_tile(gates, rem, T);
-  for (int it = 0; it < 64; ++it) {
-    uint64_t bestT = 0;
-    const uint64_t outs = full & ~T;
-    if (popc(T) < k) {
-      for (uint64_t o = outs; o; o &= o - 1) {
-        const uint64_t t2 = T | (o & -o);
-        const int sc = score_tile(gates, rem, t2);
-        if (sc > best) best = sc, bestT = t2;
-      }
-    } else {
-      for (uint64_t i = T & ~fixed; i; i &= i - 1)
+  // hill climbing over single-bit additions / exchanges (bits of `fixed` stay)
+  auto climb = [&](uint64_t T0, int& sc0) {
+    uint64_t Tc = T0;
+    int best = score_tile(gates, rem, Tc);
+    for (int it = 0; it < 64; ++it) {
+      uint64_t bestT = 0;
+      const uint64_t outs = full & ~Tc;
+      if (popc(Tc) < k) {
         for (uint64_t o = outs; o; o &= o - 1) {
-          const uint64_t t2 = (T & ~(i & -i)) | (o & -o);
+          const uint64_t t2 = Tc | (o & -o);
           const int sc = score_tile(gates, rem, t2);
           if (sc > best) best = sc, bestT = t2;
         }
+      } else {
+        for (uint64_t i = Tc & ~fixed; i; i &= i - 1)
+          for (uint64_t o = outs; o; o &= o - 1) {
+            const uint64_t t2 = (Tc & ~(i & -i)) | (o & -o);
+            const int sc = score_tile(gates, rem, t2);
+            if (sc > best) best = sc, bestT = t2;
+          }
+      }
+      if (!bestT) break;
+      Tc = bestT;
     }
-    if (!bestT) break;
-    T = bestT;
+    sc0 = best;
+    return Tc;
+  };
+  int best;
+  uint64_t bestT = climb(T, best);
+  if (seeds) {
+    // more starting points: every window of consecutive free bits (1-D
+    // brickwork circuits want contiguous qubit ranges), seeds == 1: the best
+    // window is climbed; seeds == 2: every window is climbed
+    const int free_k = k - popc(fixed);
+    uint64_t bw = 0;
+    int bws = -1;
+    for (int a = 0; a + free_k <= n && free_k > 0; ++a) {
+      uint64_t W = fixed;
+      int got = 0;
+      for (int b = a; b < n && got < free_k; ++b)
+        if (!((fixed >> b) & 1ull)) {
+          W |= 1ull << b;
+          ++got;
+        }
+      if (got < free_k) break;
+      if (seeds >= 2) {
+        int sc;
+        const uint64_t Tc = climb(W, sc);
+        if (sc > best) best = sc, bestT = Tc;
+      } else {
+        const int sc = score_tile(gates, rem, W);
+        if (sc > bws) bws = sc, bw = W;
+      }
+    }
+    if (seeds == 1 && bws >= 0) {
+      int sc;
+      const uint64_t Tc = climb(bw, sc);
+      if (sc > best) best = sc, bestT = Tc;
+    }
   }
-  return T;
+  return bestT;
 }
 
 }  // namespace
@@ -712,7 +752,9 @@ std::vector<std::pair<int, int>> remap_swaps(const std::vector<int>& perm, uint6
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, bool remap, double flops_budget) {
+FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, bool remap, double flops_budget,
+                     int seeds) {
+  if (seeds < 0) seeds = getenv("QC_PLAN_SEEDS") ? atoi(getenv("QC_PLAN_SEEDS")) : 0;
   FusedPlan plan;
   std::vector<PGate> gates = gates_in;  // bits relabelled by in-pass remap swaps
   plan.perm.resize(n);
@@ -723,7 +765,7 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
 
   while (!remaining.empty()) {
     // search: the tile set is fixed before the take scan (row bits always in it)
-    const uint64_t Tc = (remap && n > k) ? choose_tile(gates, remaining, rows, k, n) : ~0ull;
+    const uint64_t Tc = (remap && n > k) ? choose_tile(gates, remaining, rows, k, n, seeds) : ~0ull;
     uint64_t T = rows;
     uint64_t blocked = 0;
     size_t bytes = 0;
@@ -767,7 +809,7 @@ FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates_in, b
     // inside a sub-stage) -- and relabel the deferred gates accordingly.
     std::vector<std::pair<int, int>> swaps;
     uint64_t W = 0;
-    if (remap && n > k && !deferred.empty()) W = choose_tile(gates, deferred, 0, k, n);
+    if (remap && n > k && !deferred.empty()) W = choose_tile(gates, deferred, 0, k, n, seeds);
     // last pass: bring every displaced bit home (same layout in and out, so a
     // repeated circuit reuses its plan, JIT kernels and CUDA graph)
     uint64_t D = 0;  // displaced positions (padding with them lets items go home)

@@ -102,8 +102,11 @@ struct FusedPlan {
 // remap: passes may end with swaps of row bits and tile bits (plan.perm).
 // flops_budget > 0: a pass stops taking gates once their algorithmic flops per
 // amplitude (gate_flops) would exceed it (the HBM/ALU ridge of a pass).
+// seeds: tile-choice starting points (choose_tile): 0 the in-order greedy
+// tile, 1 also the best window of consecutive bits, 2 every such window (each
+// hill-climbed); -1: QC_PLAN_SEEDS (default 0).
 FusedPlan plan_fused(int n, int k, int rb, const std::vector<PGate>& gates, bool remap = false,
-                     double flops_budget = 0);
+                     double flops_budget = 0, int seeds = -1);
 // Algorithmic flops per amplitude of the fused plan (ALU roofline numerator).
 double plan_flops_per_amp(const FusedPlan& plan);
 double pass_flops_per_amp(const FusedPassPlan& pp);
