@@ -300,7 +300,8 @@ qc_status qc_state_write(qc_state* s, uint64_t first, uint64_t count, const void
  * the read-back of chunk c+1 -- PCIe / C2C links are full duplex, so handing
  * a result back and loading the next input costs about one direction.  Chunk
  * c is uploaded only after it has been read, so host_src == host_dst uploads
- * exactly what was read.  Blocks.  Same range / layout rules as
+ * exactly what was read (the two buffers must be identical or disjoint).
+ * Blocks.  Same range / layout rules as
  * qc_state_read (a non-canonical single-GPU layout: read, then write). */
 qc_status qc_state_readwrite(qc_state* s, uint64_t first, uint64_t count, void* host_dst, const void* host_src);
 

@@ -966,6 +966,12 @@ qc_status qc_state_readwrite(qc_state* s, uint64_t first, uint64_t count, void* 
   if (st != QC_OK) return st;
   const uint64_t N = 1ull << s->n;
   if ((!host_dst || !host_src) && count) return fail(QC_ERR_INVALID_ARG, "host buffer is NULL");
+  {
+    const size_t nb = count * amp_bytes(s);
+    const char *d0 = (const char*)host_dst, *s0 = (const char*)host_src;
+    if (d0 != s0 && d0 < s0 + nb && s0 < d0 + nb)
+      return fail(QC_ERR_INVALID_ARG, "host_dst and host_src overlap partially (must be identical or disjoint)");
+  }
   if (first > N || count > N - first)
     return fail(QC_ERR_INVALID_ARG, "range [%llu,+%llu) exceeds 2^%d", (unsigned long long)first,
                 (unsigned long long)count, s->n);
