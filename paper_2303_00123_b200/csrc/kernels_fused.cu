@@ -415,8 +415,15 @@ bool make_row_tmap(void* base, int n, int rb, bool dbl, QcTmap* out) {
   if (!enc) return false;
   const uint64_t elems = (uint64_t)(dbl ? 2 : 1) << rb;
   // Rows above 1 KiB (8 KiB per gather4 request) deadlocked intermittently
-  // under load on B200 (DESIGN "gather4 row limit"): use the row path there.
-  if (elems * 8 > 1024 || n - rb > 31 || n - rb < 2) return false;
+  // under load on B200 in round 1, before the per-buffer tile tags of the
+  // ring (fused_types.h).  Round 2 re-tested 2 KiB rows with the cap lifted
+  // (QC_GATHER4_MAX_ROW=2048: 288 stress runs, c128 + c64, no hang, parity
+  // green -- profiles/round2_stress_gather4_2k.log): the hang was the
+  // parity aliasing the tags fixed.  The cap stays because the default box
+  // transport never wants gather4 rows that wide.
+  static const uint64_t max_row = getenv("QC_GATHER4_MAX_ROW") ? strtoull(getenv("QC_GATHER4_MAX_ROW"), nullptr, 10)
+                                                                  : 1024;
+  if (elems * 8 > max_row || elems > 256 || n - rb > 31 || n - rb < 2) return false;
   cuuint64_t gdim[2] = {elems, (cuuint64_t)1 << (n - rb)};
   cuuint64_t gstride[1] = {elems * 8};
   cuuint32_t box[2] = {(cuuint32_t)elems, 1};
