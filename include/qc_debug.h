@@ -60,6 +60,14 @@ qc_status qc_debug_dist_schedule(int n, int world, int relabel, const qc_gate* o
 qc_status qc_debug_dist_schedule_ex(int n, int world, int relabel, int exchange_mode, const qc_gate* ops,
                                     size_t n_ops, int* steps, int max_steps, int* n_steps, int* layout_out);
 
+/* Group plans (QC_OPT_EXCHANGE 3, host arithmetic): for a pass with tile bit
+ * set T over an n-bit index sharded over `world` ranks (rank bits n-p..n-1),
+ * rank `rank`'s tile range [tile0, tile0+count) of the pass's 2^(n-|T|)
+ * tiles, the number j of rank bits in T, and owners[h] = the rank holding
+ * sub-tile h (its T-rank bits = h) for h < 2^j (-1 beyond). */
+qc_status qc_debug_group_split(int n, int world, uint64_t tile_bits_set, int rank, uint64_t* tile0,
+                               uint64_t* count, int* j, int* owners);
+
 /* Run one qubit-swap exchange of physical rank bit g with local bit l on a
  * sharded state (collective; enqueued on the state's stream); the layout is
  * updated.  Used to time NVLink exchanges in isolation. */

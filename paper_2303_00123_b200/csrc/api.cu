@@ -1238,6 +1238,21 @@ extern "C" qc_status qc_debug_dist_schedule_ex(int n, int world, int relabel, in
   return QC_OK;
 }
 
+extern "C" qc_status qc_debug_group_split(int n, int world, uint64_t tile_bits_set, int rank, uint64_t* tile0,
+                                         uint64_t* count, int* j, int* owners) {
+  if (world < 2 || (world & (world - 1)) || n < 2 || n > 62 || rank < 0 || rank >= world || !tile0 || !count ||
+      !j || !owners)
+    return fail(QC_ERR_INVALID_ARG, "bad arguments");
+  const int p = std::countr_zero((unsigned)world), nl = n - p, k = std::popcount(tile_bits_set);
+  if ((tile_bits_set >> n) || k > nl || nl < 1) return fail(QC_ERR_INVALID_ARG, "bad tile bit set");
+  const GroupSplit sp = group_split(nl, p, tile_bits_set, 1ull << (n - k), rank);
+  *tile0 = sp.tile0;
+  *count = sp.count;
+  *j = sp.j;
+  for (int h = 0; h < 8; ++h) owners[h] = sp.owner[h];
+  return QC_OK;
+}
+
 extern "C" qc_status qc_debug_exchange(qc_state* s, int g, int l) {
   qc_status st = check_state(s);
   if (st != QC_OK) return st;

@@ -721,6 +721,42 @@ qc_status world_barrier(qc_state* s) {
   return r ? nccl_fail(s, r, "world barrier") : QC_OK;
 }
 
+}  // namespace
+
+// Tile split of one group-plan pass for rank r (host arithmetic, also
+// qc_debug_group_split).  T: the pass's tile bit set over the n-bit index;
+// rank bits are nl..nl+p-1.  G = the rank bits in T (j of them: the tile's
+// top j local bits), O = the other rank bits (the top p-j tile-index bits,
+// outer positions ascending).  Rank r takes the n_tiles / 2^p tiles whose
+// O bits equal r's and whose next j index bits equal r's G bits; sub-tile h
+// (G bits = h) of such a tile lives in rank owner[h] (r's O bits, G bits h).
+GroupSplit group_split(int nl, int p, uint64_t T, uint64_t n_tiles, int r) {
+  auto pext = [](uint32_t x, uint32_t m) {
+    uint32_t v = 0;
+    for (int b = 0, o = 0; b < 32; ++b)
+      if ((m >> b) & 1u) v |= ((x >> b) & 1u) << o++;
+    return v;
+  };
+  auto pdep = [](uint32_t x, uint32_t m) {
+    uint32_t v = 0;
+    for (int b = 0, o = 0; b < 32; ++b)
+      if ((m >> b) & 1u) v |= ((x >> o++) & 1u) << b;
+    return v;
+  };
+  const uint32_t all = (1u << p) - 1u;
+  const uint32_t G = (uint32_t)(T >> nl) & all;
+  GroupSplit sp;
+  sp.j = std::popcount(G);
+  const int tb = std::countr_zero(n_tiles);
+  sp.count = n_tiles >> p;
+  sp.tile0 = ((uint64_t)pext((uint32_t)r, all & ~G) << (tb - (p - sp.j))) |
+             ((uint64_t)pext((uint32_t)r, G) << (tb - p));
+  for (int h = 0; h < 8; ++h) sp.owner[h] = h < (1 << sp.j) ? (int)(((uint32_t)r & ~G) | pdep((uint32_t)h, G)) : -1;
+  return sp;
+}
+
+namespace {
+
 // A group plan (kind 3) over all n bits.  Pass i on rank r: the tile's rank
 // bits G (|G| = j) are its top j local bits; the other rank bits O are the
 // top p-j tile-index bits.  Rank r takes the tiles whose O bits equal its own
@@ -739,26 +775,12 @@ qc_status enqueue_group_plan(qc_state* s, const DistPlan::Step& st) {
   auto map_of = [&](int q, size_t i) -> const QcTmap& {
     return e->passes[i].g4 == 2 ? e->vr_box[(size_t)q][i] : e->vr_row[(size_t)q];
   };
-  auto pext = [](uint32_t x, uint32_t m) {
-    uint32_t r = 0;
-    for (int b = 0, o = 0; b < 32; ++b)
-      if ((m >> b) & 1u) r |= ((x >> b) & 1u) << o++;
-    return r;
-  };
-  auto pdep = [](uint32_t x, uint32_t m) {
-    uint32_t r = 0;
-    for (int b = 0, o = 0; b < 32; ++b)
-      if ((m >> b) & 1u) r |= ((x >> o++) & 1u) << b;
-    return r;
-  };
-  const uint32_t all = (1u << p) - 1u;
   auto launch_rank = [&](int r, size_t i) -> int {
     PassDesc pd = e->passes[i];
-    const uint32_t G = (uint32_t)(pass_tile_set(pd) >> nl) & all;
-    const int j = std::popcount(G);
-    const int tb = std::countr_zero(pd.n_tiles);
-    pd.n_tiles >>= p;
-    pd.tile0 = ((uint64_t)pext((uint32_t)r, all & ~G) << (tb - (p - j))) | ((uint64_t)pext((uint32_t)r, G) << (tb - p));
+    const GroupSplit sp = group_split(nl, p, pass_tile_set(pd), pd.n_tiles, r);
+    const int j = sp.j;
+    pd.n_tiles = sp.count;
+    pd.tile0 = sp.tile0;
     pd.rank_bits = 0;
     pd.addr_bits = 0;
     QcTmapSet tms;
@@ -766,13 +788,12 @@ qc_status enqueue_group_plan(qc_state* s, const DistPlan::Step& st) {
       tms.m[0] = map_of(r, i);
       return launch_pass(s, e, i, pd, buf_of(r), tms, s->stream);
     }
-    for (uint32_t h = 0; h < (1u << j); ++h) {
-      const int q = (int)(((uint32_t)r & ~G) | pdep(h, G));
-      tms.m[h] = map_of(q, i);
+    for (int h = 0; h < (1 << j); ++h) {
+      tms.m[h] = map_of(sp.owner[h], i);
       pd.sub_addr[h] = 0;
-      pd.sub_state[h] = (uint64_t)(uintptr_t)buf_of(q);
+      pd.sub_state[h] = (uint64_t)(uintptr_t)buf_of(sp.owner[h]);
     }
-    return launch_pass(s, e, i, pd, buf_of((int)((uint32_t)r & ~G)), tms, s->stream);
+    return launch_pass(s, e, i, pd, buf_of(sp.owner[0]), tms, s->stream);
   };
   const size_t np = e->passes.size();
   if (s->dist == 1) {

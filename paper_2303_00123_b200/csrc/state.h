@@ -100,6 +100,12 @@ void dist_release(qc_state* s);  // drop sharded plans + communicator
 qc_status dist_schedule_dry(int n, int world, int relabel, const qc_gate* ops, size_t n_ops,
                             std::vector<int>& out, std::vector<int>& layout_out, const MTable* mt = nullptr,
                             int xmode = 0);
+struct GroupSplit {
+  uint64_t tile0 = 0, count = 0;  // this rank's tile range of the pass
+  int j = 0;                      // rank bits in the tile
+  int owner[8] = {};              // rank holding sub-tile h (h < 2^j)
+};
+GroupSplit group_split(int nl, int p, uint64_t T, uint64_t n_tiles, int r);
 struct ExchangeRun {
   uint64_t offset;  // amplitudes, within the shard
   uint64_t count;

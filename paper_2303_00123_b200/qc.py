@@ -87,6 +87,7 @@ class qc_plan_stats(ctypes.Structure):
 
 
 DEBUG_EXPORTS = ["qc_debug_plan", "qc_debug_exchange_runs", "qc_debug_dist_schedule", "qc_debug_dist_schedule_ex", "qc_debug_exchange",
+                 "qc_debug_group_split",
                  "qc_debug_fma_peak", "qc_debug_box_layout"]
 
 _lib = None
@@ -134,6 +135,10 @@ def lib() -> ctypes.CDLL:
     L.qc_debug_dist_schedule.restype = ctypes.c_int
     L.qc_debug_dist_schedule_ex.argtypes = [i32, i32, i32, i32, vp, sz, vp, i32, ctypes.POINTER(ctypes.c_int), vp]
     L.qc_debug_dist_schedule_ex.restype = ctypes.c_int
+    L.qc_debug_group_split.argtypes = [i32, i32, u64, i32, ctypes.POINTER(ctypes.c_uint64),
+                                       ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int),
+                                       ctypes.POINTER(ctypes.c_int)]
+    L.qc_debug_group_split.restype = ctypes.c_int
     L.qc_debug_exchange.argtypes = [vp, i32, i32]
     L.qc_debug_exchange.restype = ctypes.c_int
     L.qc_debug_box_layout.argtypes = [u64, i32, i32, ctypes.POINTER(ctypes.c_int), vp, vp,
@@ -456,6 +461,15 @@ def debug_dist_schedule(n: int, world: int, ops, relabel: bool = True, exchange:
                                         len(arr), steps.ctypes.data, cap, ctypes.byref(ns), lay.ctypes.data))
     out = [tuple(int(x) for x in steps[4 * i:4 * i + 4]) for i in range(min(ns.value, cap))]
     return out, [int(x) for x in lay[:n]]
+
+
+def debug_group_split(n: int, world: int, tile_bits_set: int, rank: int):
+    """Group-plan tile split of one pass (host): (tile0, count, j, owners)."""
+    t0, cnt, j = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int()
+    own = (ctypes.c_int * 8)()
+    _check(lib().qc_debug_group_split(n, world, tile_bits_set, rank, ctypes.byref(t0), ctypes.byref(cnt),
+                                      ctypes.byref(j), own))
+    return t0.value, cnt.value, j.value, [own[h] for h in range(1 << j.value)]
 
 
 def version() -> str:

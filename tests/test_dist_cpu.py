@@ -216,3 +216,82 @@ def test_group_plan_schedule():
                 a, b = op.qubits
                 want[a], want[b] = want[b], want[a]
         assert lay == want
+
+
+def _group_worker(rank, world, port, cases, q):
+    """Emulate group-plan passes over gloo: every rank processes its tile
+    range of each pass (qc_debug_group_split), fetching each tile's sub-tiles
+    from their owner ranks and writing the result back to them; the pass
+    applied here is the permutation x -> x XOR T of the global index (it
+    touches every amplitude of every tile exactly once)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ok = True
+        for n, T in cases:
+            p = world.bit_length() - 1
+            nl = n - p
+            rng = np.random.default_rng(n * 131 + T % 9973)
+            glob = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n))
+            shard = torch.from_numpy(glob[rank << nl:(rank + 1) << nl].copy())
+            # all shards visible (stands in for the IPC-mapped peer buffers)
+            shards = [torch.zeros_like(shard) for _ in range(world)]
+            dist.all_gather(shards, shard)
+            t0, cnt, j, owners = qc.debug_group_split(n, world, T, rank)
+            tpos = [b for b in range(n) if (T >> b) & 1]
+            opos = [b for b in range(n) if not (T >> b) & 1]
+            rank_t = [b for b in tpos if b >= nl]
+            writes = []  # (owner, local index, value)
+            for t in range(t0, t0 + cnt):
+                base = sum(((t >> i) & 1) << b for i, b in enumerate(opos))
+                for x in range(1 << len(tpos)):
+                    g = base | sum(((x >> i) & 1) << b for i, b in enumerate(tpos))
+                    h = sum(((g >> b) & 1) << i for i, b in enumerate(rank_t))
+                    own = owners[h]
+                    if own != (g >> nl):  # the owner of sub-tile h holds the amplitude
+                        ok = False
+                    src = g ^ T  # the pass: out[g] = in[g ^ T] (same tile: T bits flipped)
+                    writes.append((own, g & ((1 << nl) - 1), shards[src >> nl][src & ((1 << nl) - 1)].item()))
+            gathered = [None] * world
+            dist.all_gather_object(gathered, writes)
+            mine = np.full(1 << nl, np.nan + 0j)
+            seen = np.zeros(1 << nl, dtype=np.int64)
+            for w in gathered:
+                for own, li, v in w:
+                    if own == rank:
+                        mine[li] = v
+                        seen[li] += 1
+            idx = np.arange(rank << nl, (rank + 1) << nl)
+            ok = ok and bool(np.all(seen == 1)) and bool(np.allclose(mine, glob[idx ^ T]))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_group_plan_tile_split_over_gloo(world):
+    """Host logic of group plans (QC_OPT_EXCHANGE 3) with real multi-process
+    communication: each rank's tile range and sub-tile owners, for passes
+    whose tile holds 0, 1 or all rank bits, cover every amplitude exactly once
+    and move it between the right shards."""
+    n = 10
+    p = world.bit_length() - 1
+    nl = n - p
+    low = (1 << 3) - 1  # row bits 0..2
+    cases = [(n, low | (1 << 5)),                         # no rank bit: local tiles
+             (n, low | (1 << (n - 1))),                   # the top rank bit
+             (n, low | (1 << 6) | (((1 << p) - 1) << nl))]  # every rank bit
+    if p > 1:
+        cases.append((n, low | (1 << nl)))                # the lowest rank bit only
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_group_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, ok in res:
+        assert ok, f"rank {rank}: group-plan tile split / owners wrong"
