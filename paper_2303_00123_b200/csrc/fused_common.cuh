@@ -95,18 +95,45 @@ __device__ __forceinline__ void qc_scatter4(const QcTmap* tm, int32_t r0, int32_
 }
 // One 5-D TMA box (the whole tile) per request: dims in ascending physical
 // bit order, so the box lands in smem in tile-local index order.
+// L2 cache hints of the box transport (experiment knob, JIT passes only:
+// QC_L2_HINT 1 = evict_first on tile loads and stores -- the state streams
+// through L2 once per pass).
+#ifndef QC_L2_HINT
+#define QC_L2_HINT 0
+#endif
+__device__ __forceinline__ uint64_t qc_l2_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void qc_box_load(void* dst, const QcTmap* tm, const int32_t (&c)[5], uint64_t* bar) {
+#if QC_L2_HINT
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(qc_saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(bar)),
+      "l"(qc_l2_policy())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(qc_saddr(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(bar))
       : "memory");
+#endif
 }
 __device__ __forceinline__ void qc_box_store(const QcTmap* tm, const int32_t (&c)[5], const void* src) {
+#if QC_L2_HINT
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4, %5}], [%6], %7;"
+               ::"l"(reinterpret_cast<uint64_t>(tm)),
+               "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(src)), "l"(qc_l2_policy())
+               : "memory");
+#else
   asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
                    reinterpret_cast<uint64_t>(tm)),
                "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(qc_saddr(src))
                : "memory");
+#endif
 }
 // Box coordinates of a tile: per dim, the outer bits above its tile run
 // (dim 0 in f64 elements: 2 per complex128 amplitude, 1 per complex64).
