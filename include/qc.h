@@ -119,8 +119,9 @@ typedef enum {
     QC_OPT_REMAP = 9,         /* 1 (default): a fused pass may end by swapping row bits with
                                  tile bits the next pass needs (a relabel, like SWAP);
                                  0: the row bits keep their qubits                           */
-    QC_OPT_EXCHANGE = 10      /* NCCL-sharded states, qubit-swap exchange backend (collective:
-                                 set the same value on every rank):
+    QC_OPT_EXCHANGE = 10      /* sharded states (NCCL, and the loopback, which runs the same
+                                 schedules on one GPU), how gates on rank-bit qubits are
+                                 served (collective: set the same value on every rank):
                                  0 (default): NCCL send/recv of 256 MiB chunks into two
                                    ping-pong staging buffers on a second stream, each chunk's
                                    copy into place overlapping the next chunk's transfer;
