@@ -420,6 +420,11 @@ __device__ __forceinline__ void qc_prun_slot(C (&v)[kSlots], const C w0, const C
 }
 
 // ------------------------------------------------------- tile pipeline
+// QC_WARP_SYNC 1: consumers poll the buffer tag and arrive on the `empty`
+// barrier once per warp (after __syncwarp) instead of once per thread.
+#ifndef QC_WARP_SYNC
+#define QC_WARP_SYNC 0
+#endif
 // Body must provide:
 //   static size_t smem_bytes(const PassDesc&)          extra smem it needs
 //   void setup(unsigned char* extra, const PassDesc&)   all threads, before sync
@@ -460,7 +465,7 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
   if (tid == 0) {
     for (int b = 0; b < NBUF; ++b) {
       qc_mbar_init(&full[b], 1);
-      qc_mbar_init(&empty[b], kGroupThreads);
+      qc_mbar_init(&empty[b], QC_WARP_SYNC ? kGroupThreads / 32 : kGroupThreads);
       buf_tile[b] = 0xffffffffu;
     }
     qc_fence_mbar_init();
@@ -581,12 +586,24 @@ __device__ __forceinline__ void qc_fused_pipeline(C* __restrict__ state, const P
     body.prologue(tbase, par);
     if (kGroups > 1 && NBUF % kGroups) {
       // wait until the producer has claimed buffer b for this tile (see fused_types.h)
+#if QC_WARP_SYNC
+      // one poller per warp (32x fewer atomics on the tag word)
+      if ((threadIdx.x & 31) == 0)
+        while (atomicOr(const_cast<uint32_t*>(&buf_tile[b]), 0u) != (uint32_t)i) __nanosleep(64);
+      __syncwarp();
+#else
       while (atomicOr(const_cast<uint32_t*>(&buf_tile[b]), 0u) != (uint32_t)i) __nanosleep(64);
+#endif
     }
     qc_mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1ull));
     body.tile(bufs + (size_t)b * buf_amps, tbase, par);
     qc_fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+#if QC_WARP_SYNC
+    __syncwarp();            // the warp's fenced writes precede lane 0's (release) arrive
+    if ((threadIdx.x & 31) == 0) qc_mbar_arrive(&empty[b]);
+#else
     qc_mbar_arrive(&empty[b]);
+#endif
   }
 }
 
