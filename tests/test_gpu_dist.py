@@ -188,3 +188,20 @@ def test_group_plan_permutation_bit_exact(qcmod):
     ops = qcgen.random_circuit(n, 200, seed=29, kinds=("X", "CNOT", "SWAP", "CCX"))
     got, info = run_lb(qcmod, n, "c128", world, ops, exchange=3)
     assert np.array_equal(got, ref(n, "c128", ops))
+
+
+@pytest.mark.parametrize("xmode", [0, 2, 3])
+@pytest.mark.parametrize("world,n", [(2, 9), (2, 10), (4, 10), (4, 11), (8, 11), (8, 12)])
+def test_smallest_sharded_states(qcmod, xmode, world, n):
+    """The smallest shards allowed (8-10 local qubits: tiles smaller than the
+    default, few tiles per pass, the group-plan tile split at its minimum)."""
+    ops = qcgen.random_circuit(n, 60, seed=3 * n + world) + qcgen.qft(n)
+    got, info = run_lb(qcmod, n, "c128", world, ops, reps=2, exchange=xmode)
+    assert maxerr(got, ref(n, "c128", ops, reps=2)) <= 1e-12
+
+
+def test_shards_below_8_local_qubits_rejected(qcmod):
+    from paper_2303_00123_b200 import QCError
+    with pytest.raises(QCError) as e:
+        qcmod.State.loopback(9, "c128", 4)
+    assert e.value.status == 1 and "8 local qubits" in str(e.value)
