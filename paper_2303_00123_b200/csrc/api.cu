@@ -392,7 +392,7 @@ qc_status build_fused_entry(qc_state* s, const std::vector<PGate>& gates, int n_
   const int tbits = tmap_bits ? tmap_bits : n_plan;
   const bool g4 = (s->tma_mode == 0 || s->tma_mode == 2) && make_row_tmap(tb, tbits, rb, s->dbl, &e->tmap) &&
                   (!peer_base || make_row_tmap(peer_base, tbits, rb, s->dbl, &e->tmap_peer));
-  e->pair_mask = group_mask;
+  e->group_mask = group_mask;
   for (auto& p : fp.passes) {
     p.desc.g4 = g4 ? 1 : 0;
     p.desc.pshift = g4 ? 31 : rb;  // TMA tensor smem dst must be 128-B aligned: no padding

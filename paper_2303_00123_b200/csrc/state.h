@@ -24,8 +24,8 @@ struct PlanEntry {
   int jit_state = 0;                 // 0 not tried, 1 built, -1 failed
   QcTmap tmap{};                     // row tensor map (gather4 / scatter4 path)
   std::vector<QcTmap> tmaps;         // per-pass box tensor maps (PassDesc g4 == 2; empty otherwise)
-  // pair segments (dist.cu, QC_OPT_EXCHANGE 2): plan bit n_loc is a rank bit
-  uint64_t pair_mask = 0;            // the pair bit (plan space); 0: not a pair segment
+  // plans spanning shards (dist.cu, QC_OPT_EXCHANGE 2 / 3): rank bits in the plan
+  uint64_t group_mask = 0;           // plan bits that are rank bits (pair / group plans); 0: none
   QcTmap tmap_peer{};                // the partner's buffer (P2P): row tensor map ...
   std::vector<QcTmap> tmaps_peer;    // ... and per-pass box tensor maps
   // loopback pair segments: tensor maps over each virtual rank's own shard
