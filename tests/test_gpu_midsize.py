@@ -71,3 +71,29 @@ def test_timed_configuration_matches_oracle(qcmod, case, prec):
     print(f"{case} {prec}: passes={info['last_passes']} max|err|={err:.3e} rel_L2={rel:.3e}")
     assert err <= TOL[prec], (err, rel)
     assert rel <= REL_L2[prec], (err, rel)
+
+
+@pytest.mark.parametrize("xmode,world", [(3, 8), (3, 2), (2, 4), (0, 8)])
+@pytest.mark.parametrize("case", ["tfxy24_s10", "qft24", "random24_300"])
+def test_sharded_loopback_matches_oracle(qcmod, case, xmode, world):
+    """The sharded path at n = 24 (shards of 2^21-2^23 amplitudes: rings wrap,
+    16-warp kernels at steady state) in every exchange mode, element-wise
+    against the oracle after U.U^-1.U (the 3rd run: NVRTC plans reused)."""
+    n = 24
+    ops = {"tfxy24_s10": qcgen.tfxy(n, 10), "qft24": qcgen.qft(n),
+           "random24_300": qcgen.random_circuit(n, 300, seed=77)}[case]
+    inv = qcgen.inverse(ops)
+    with qcmod.State.loopback(n, "c128", world) as s:
+        s.set_option("exchange", xmode)
+        s.init_random(qcgen.STATE_SEED)
+        s.run(ops)
+        s.run(inv)
+        s.run(ops)
+        info = s.info()
+        got = s.read()
+    ref = oracle.run(n, qcgen.random_state(n), ops)
+    err = float(np.abs(got - ref).max())
+    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    print(f"{case} mode {xmode} x{world}: passes={info['last_passes']} exchanges={info['last_exchanges']} "
+          f"spanning={info['last_pair_segments']} max|err|={err:.3e} rel_L2={rel:.3e}")
+    assert err <= TOL["c128"] and rel <= REL_L2["c128"], (err, rel)
